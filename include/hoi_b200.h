@@ -1,0 +1,194 @@
+/*
+ * hoi_b200.h -- C ABI of libhoib200.so, the B200 (sm_100a) engine behind the
+ * n-plet higher-order-interaction hot path.
+ *
+ * The reference (/root/reference/pkg/src/hoi) is a pure-Python package and
+ * has no FFI of its own.  Each entry point below replaces one numeric stage
+ * of its hot path; the citation names the reference function whose
+ * behaviour it carries (ref:<file>:<line>).  The Python host layer
+ * (paper_2501_03381_b200/) keeps the reference's Python signatures and calls
+ * these through ctypes (see INTEGRATION.md for the binding).
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless named h_*;
+ *     buffers are caller-allocated, the library never allocates in a hot
+ *     call except inside an explicit workspace argument;
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     asynchronous on that stream unless documented otherwise;
+ *   - calls on different streams/devices are reentrant; the only global
+ *     state is a thread-local last-error string;
+ *   - return value is an HOI_* status code.
+ *
+ * Layouts
+ *   corr    (N, N, D) float64, dataset index fastest: corr[(i*N + j)*D + d]
+ *           is the correlation form R = D^-1/2 Sigma D^-1/2 of dataset d
+ *           (unit diagonal, exactly symmetric);
+ *   sdiag   (D, N) float64, the covariance diagonal Sigma_jj (jitter scale);
+ *   eta     (D, kstride) float64 finite-sample bias table eta(k, T_d) or NULL
+ *           (ref:copula_core.py:234-244);
+ *   out     4 planes of (B, D) float64: tc, dtc, o, s, plane stride B*D
+ *           (the HoiBatch layout, ref:measures.py:18-27).
+ */
+#ifndef HOI_B200_H
+#define HOI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HOI_OK = 0,
+  HOI_INVALID_ARG = 1,          /* -> InvalidData / InvalidNplet            */
+  HOI_INSUFFICIENT_SAMPLES = 2, /* -> InsufficientSamples                   */
+  HOI_NOT_PD = 3,               /* -> NotPositiveDefinite (see err buffers) */
+  HOI_CUDA_ERROR = 4,
+  HOI_CAPACITY = 5              /* workspace / output too small             */
+};
+
+/* Library version (major*10000 + minor*100 + patch). */
+int hoi_version(void);
+
+/* Last error message of the calling thread ("" if none). */
+const char *hoi_last_error(void);
+
+/* Number of kernels this library launched from the calling process
+ * (monotone counter; used by bench.py's gpu_launches and by tests). */
+int64_t hoi_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * (1) Gaussian copula + covariance.
+ * ------------------------------------------------------------------------- */
+
+/* Ordinal per-column ranks with ties broken by row (stable) and the copula
+ * values z = qgrid[rank-1].  Replaces rank_columns + copula_transform
+ * (ref:copula_core.py:155-174).
+ *   x      (D, T, N) float64 row-major data (already validated/finite);
+ *   qgrid  (T,) float64 = ndtri((1..T)/(T+1)) computed on the host with the
+ *          reference's scipy routine, so z is bit-identical to the reference;
+ *   ranks  (D, T, N) int64 output, 1-based, or NULL;
+ *   z      (D, T, N) float64 output;
+ *   ws     device workspace of ws_bytes (query with ws == NULL: the required
+ *          size is written to *ws_bytes and HOI_OK returned). */
+int hoi_rank_copula(const double *x, int64_t T, int32_t N, int32_t D,
+                    const double *qgrid, int64_t *ranks, double *z,
+                    void *ws, size_t *ws_bytes, void *stream);
+
+/* Unbiased covariance (divisor T-1) of centred columns, upper triangle
+ * computed once and mirrored so cov == cov^T exactly.  Replaces
+ * estimate_covariance (ref:copula_core.py:177-189).
+ *   z (D, T, N) float64 -> cov (D, N, N) float64. */
+int hoi_covariance(const double *z, int64_t T, int32_t N, int32_t D,
+                   double *cov, void *stream);
+
+/* Correlation form used by every measure kernel: corr (N,N,D) and sdiag (D,N)
+ * from cov (D,N,N).  The measures only depend on log det R_S and the
+ * inverse diagonal of R_S (the per-variable log Sigma_jj terms cancel in
+ * tc/dtc/o/s, ref:measures.py:41-69). */
+int hoi_correlation(const double *cov, int32_t N, int32_t D, double *corr,
+                    double *sdiag, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * (2) Batched n-plet evaluation (gather + Cholesky + inverse diagonal +
+ *     bias + TC/DTC/O/S epilogue).  Replaces extract_subcov_batch +
+ *     _batched_logdet_invdiag + entropy_terms + compute_hoi_batch for
+ *     fixed-order batches (ref:nplet_engine.py:185-201,227-330;
+ *     ref:measures.py:72-81).
+ *
+ *   idx        (B, K) int32 strictly increasing rows;
+ *   out        4 x (B, D) measures or NULL;
+ *   logdet     (B, D) log det Sigma_S or NULL         } entropy_terms compat
+ *   invdiag    (B, D, K) (Sigma_S^-1)_jj or NULL      } (ref:nplet_engine.py:312-330)
+ *   err_count  device int32 counter (caller zeroes it);
+ *   err_coords device int64 pairs (b, d) of matrices that stayed non-PD
+ *              after the reference's single jitter retry
+ *              eps = 1e-10 * trace(Sigma_S) / K (ref:nplet_engine.py:237-264);
+ *              at most err_cap pairs are stored, the counter keeps counting.
+ * ------------------------------------------------------------------------- */
+int hoi_eval_indices(const double *corr, const double *sdiag, const double *eta,
+                     int32_t kstride, int32_t N, int32_t D, const int32_t *idx,
+                     int64_t B, int32_t K, double *out, double *logdet,
+                     double *invdiag, int32_t *err_count, int64_t *err_coords,
+                     int32_t err_cap, void *stream);
+
+/* Mixed-order (mask) batches: masks (B, W) uint64 words (bit j of word j/64
+ * = variable j).  Equivalent to identity padding (ref:nplet_engine.py:204-224,
+ * 332-351): each row is compacted to its members and evaluated at its own
+ * order.  invdiag, when requested, is (B, D, N) with zeros outside the row
+ * and logdet (B, D). */
+int hoi_eval_masks(const double *corr, const double *sdiag, const double *eta,
+                   int32_t kstride, int32_t N, int32_t D, const uint64_t *masks,
+                   int32_t W, int64_t B, double *out, double *logdet,
+                   double *invdiag, int32_t *err_count, int64_t *err_coords,
+                   int32_t err_cap, void *stream);
+
+/* Raw matrix stack: (logdet, inverse diagonal) of M matrices (M, K, K) with
+ * the same jitter rule.  Replaces _batched_logdet_invdiag
+ * (ref:nplet_engine.py:267-281); err_coords hold (m, 0). */
+int hoi_logdet_invdiag(const double *mats, int64_t M, int32_t K,
+                       double *logdet, double *invdiag, int32_t *err_count,
+                       int64_t *err_coords, int32_t err_cap, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * (3) Enumeration: global order-major lexicographic rank -> k-subset
+ *     (ref:nplet_engine.py:118-136 chained at ref:scanner.py:345-347).
+ *     idx_out (count, kmax) int32 padded with -1; order_out (count,) int32.
+ *     Requires N <= 64.
+ * ------------------------------------------------------------------------- */
+int hoi_unrank(int32_t N, int32_t kmin, int32_t kmax, int64_t g_begin,
+               int64_t count, int32_t *idx_out, int32_t *order_out,
+               void *stream);
+
+/* Same for an explicit list of global ranks (TopK candidates). */
+int hoi_unrank_list(int32_t N, int32_t kmin, int32_t kmax, const int64_t *ranks,
+                    int64_t count, int32_t *idx_out, int32_t *order_out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * (4) Exhaustive scan over the global rank range [g_begin, g_end) of orders
+ *     kmin..kmax, full output: out is 4 planes of ((g_end-g_begin), D)
+ *     measures in enumeration order (the concatenation of every batch the
+ *     reference's scan would hand to its reducer, ref:scanner.py:308-365).
+ *
+ *     engine: 0 = auto, 1 = per-n-plet Cholesky (unrank + K-templated
+ *     register kernels, any N <= 64), 2 = subset-lattice engine (N <= 34:
+ *     log-det table over all 2^N subsets + leave-one-out stencil; needs the
+ *     workspace, query its size with ws == NULL).
+ * ------------------------------------------------------------------------- */
+int hoi_scan_full(const double *corr, const double *sdiag, const double *eta,
+                  int32_t kstride, int32_t N, int32_t D, int32_t kmin,
+                  int32_t kmax, int64_t g_begin, int64_t g_end, int32_t engine,
+                  double *out, int32_t *err_count, int64_t *err_coords,
+                  int32_t err_cap, void *ws, size_t *ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * (5) Device reducers over a full-output plane (ref:scanner.py:50-137).
+ * ------------------------------------------------------------------------- */
+
+/* Candidate filter for TopK: writes the positions p in [0, n) of plane
+ * `vals` (stride D, dataset d) whose key sign*vals[p*D+d] <= *thresh into
+ * cand (int64), counting into *cand_count (device int64, caller zeroes).
+ * Stores at most cand_cap positions. */
+int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d,
+                    double sign, const double *thresh, int64_t *cand,
+                    int64_t *cand_count, int64_t cand_cap, void *stream);
+
+/* Histogram with numpy.histogram semantics after clipping to [lo, hi]
+ * (ref:scanner.py:126-134): counts (D, bins) int64 accumulated. */
+int hoi_histogram(const double *vals, int64_t n, int32_t D, int32_t bins,
+                  double lo, double hi, const double *edges, int64_t *counts,
+                  void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics: FP64 pipe peak probe (the roofline denominator for the FP64
+ * kernels; MEASURED_PEAKS.json has no FP64 entry).  flops per launch =
+ * blocks * 256 * iters * 128.  out needs `blocks` doubles.
+ * ------------------------------------------------------------------------- */
+int hoi_fp64_probe(double *out, int64_t iters, int32_t blocks, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOI_B200_H */

@@ -1,0 +1,53 @@
+"""Device-resident state of a CovSet: the correlation form R (N, N, D)
+with the dataset index fastest, the covariance diagonal (D, N) and the
+finite-sample bias tables (D, kmax+1).  Built by libhoib200 kernels from
+the host covariances once per CovSet and cached on the instance."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from .copula_core import _bias_table
+from .errors import InvalidData
+
+
+class DeviceCovs:
+    def __init__(self, covs, torch):
+        self.torch = torch
+        self.n = covs.n_variables
+        self.d = covs.n_datasets
+        self.t_used = covs.samples_used()
+        sig = torch.from_numpy(np.ascontiguousarray(covs.stacked())).cuda()
+        self.cov = sig
+        self.corr = torch.empty((self.n, self.n, self.d), dtype=torch.float64, device=sig.device)
+        self.sdiag = torch.empty((self.d, self.n), dtype=torch.float64, device=sig.device)
+        nat.check(nat.lib().hoi_correlation(sig.data_ptr(), self.n, self.d, self.corr.data_ptr(),
+                                            self.sdiag.data_ptr(), nat.stream_handle(torch)),
+                  "correlation")
+        self._eta = {}
+
+    def eta(self, k_max: int):
+        """(D, k_max+1) bias table on the device (host-evaluated with scipy,
+        ref:nplet_engine.py:295-303)."""
+        if (self.t_used <= 0).any():
+            raise InvalidData("bias correction needs sample-estimated covariances "
+                              "(n_samples_used > 0)")
+        if k_max not in self._eta:
+            tab = np.stack([_bias_table(int(t), k_max) for t in self.t_used])
+            self._eta[k_max] = self.torch.from_numpy(tab).cuda()
+        return self._eta[k_max]
+
+
+def device_covs(covs) -> DeviceCovs:
+    torch = nat.torch_cuda()
+    key = (tuple(id(c.sigma) for c in covs.covs), tuple(int(c.n_samples_used) for c in covs.covs))
+    cached = getattr(covs, "_b200_state", None)
+    if cached is not None and cached[0] == key:
+        return cached[1]
+    st = DeviceCovs(covs, torch)
+    try:
+        object.__setattr__(covs, "_b200_state", (key, st))
+    except Exception:
+        pass
+    return st

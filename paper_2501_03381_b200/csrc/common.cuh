@@ -1,0 +1,85 @@
+// Shared device/host helpers for libhoib200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <atomic>
+
+#include "../../include/hoi_b200.h"
+
+namespace hoib {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int check_launch(const char *what);
+void count_launch(int n = 1);
+
+#define HOI_CHECK_ARG(cond, msg)                 \
+  do {                                           \
+    if (!(cond)) return ::hoib::fail(HOI_INVALID_ARG, msg); \
+  } while (0)
+
+// -------------------------------------------------------------- binomials --
+// C(n, m) for 0 <= n, m <= 64 in constant memory (saturated at UINT64_MAX when
+// it does not fit; callers restrict themselves to ranges that fit).
+constexpr int kBinomN = 65;
+uint64_t host_binom(int n, int m);
+void fill_binomials(uint64_t *h);   // host table, kBinomN^2 entries
+// Without relocatable device code every translation unit owns its own copy
+// of the constant table, so the uploader is instantiated per unit too.
+static __constant__ uint64_t c_binom[kBinomN * kBinomN];
+static inline void upload_binomials() {
+  static thread_local int uploaded_for = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (uploaded_for == dev) return;
+  uint64_t h[kBinomN * kBinomN];
+  fill_binomials(h);
+  cudaMemcpyToSymbol(c_binom, h, sizeof(h));
+  uploaded_for = dev;
+}
+
+__device__ __forceinline__ uint64_t binom(int n, int m) {
+  return (m < 0 || n < 0 || m > n) ? 0ull : c_binom[n * kBinomN + m];
+}
+
+// ------------------------------------------------- floating-point helpers --
+// Running product with a split-off binary exponent: the mantissa is only
+// renormalised when it leaves [1e-150, 1e150], so products of up to ~64
+// factors never overflow/underflow while exact products (an identity
+// matrix gives exactly 1) keep an exact log of 0.  One log per product.
+struct LogProd {
+  double m;
+  int e;
+  __device__ __forceinline__ void init() { m = 1.0; e = 0; }
+  __device__ __forceinline__ void mul(double x) { m *= x; }
+  __device__ __forceinline__ void renorm() {
+    double a = fabs(m);
+    if (a < 1e-150 || a > 1e150) {
+      int ex;
+      m = frexp(m, &ex);
+      e += ex;
+    }
+  }
+  __device__ __forceinline__ double log_value() const {
+    double l = log(m);
+    return e == 0 ? l : l + (double)e * 0.69314718055994530942;
+  }
+};
+
+// Order-preserving map of a double onto uint64 (-0.0 canonicalised to +0.0,
+// which is how value comparisons, and hence scipy's rankdata, treat it).
+__device__ __forceinline__ uint64_t orderable_key(double v) {
+  if (v == 0.0) v = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace hoib

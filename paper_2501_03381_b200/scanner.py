@@ -1,0 +1,554 @@
+"""Exhaustive scans with pluggable reducers (drop-in for ref:scanner.py).
+
+The n-plet space of a scan is the order-major, lexicographic sequence the
+reference enumerates (ref:scanner.py:345-347), addressed by a global rank
+g.  The device computes whole rank ranges at once (``hoi_scan_full``);
+the host then either
+
+* reduces on the device -- TopK (candidate filter + exact merge with the
+  reference's (sign*value, index tuple) key) and Histogram (numpy's edge
+  semantics) -- so only a few hundred bytes come back, or
+* replays the reference's batches (<= batch_size rows, never crossing an
+  order) to any other Reducer in enumeration order, with the same progress
+  counters.
+
+Results never depend on batch_size or workers (workers is validated and
+otherwise has nothing to do: there is no host thread pool to size).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from ._device import device_covs
+from .copula_core import CovSet
+from .errors import ExhaustiveLimitExceeded, InvalidData, InvalidOrderRange
+from .measures import HoiBatch, compute_hoi_batch
+from .nplet_engine import ERR_CAP, NpletBatch, _err_buffers, _raise_not_pd, count_nplets
+
+MEASURES = ("tc", "dtc", "o", "s")
+
+
+class Reducer:
+    """Consumes (NpletBatch, HoiBatch) pairs in enumeration order (ref:scanner.py:27-34)."""
+
+    def update(self, batch: NpletBatch, hoi: HoiBatch) -> None:
+        raise NotImplementedError
+
+    def finalize(self):
+        raise NotImplementedError
+
+
+@dataclass(frozen=True)
+class TopEntry:
+    """One selected n-plet with all four measures (ref:scanner.py:37-47)."""
+
+    indices: tuple
+    order: int
+    value: float
+    tc: float
+    dtc: float
+    o: float
+    s: float
+
+
+class TopK(Reducer):
+    """k best n-plets per dataset for one measure; ties broken by the
+    lexicographically smallest index tuple (ref:scanner.py:50-105)."""
+
+    def __init__(self, measure: str, direction: str, k: int):
+        if measure not in MEASURES:
+            raise InvalidData(f"measure must be one of {MEASURES}, got {measure!r}")
+        if direction not in ("max", "min"):
+            raise InvalidData(f"direction must be 'max' or 'min', got {direction!r}")
+        if k < 1:
+            raise InvalidData(f"k must be >= 1, got {k}")
+        self.measure, self.direction, self.k = measure, direction, k
+        self._best = None
+
+    @property
+    def sign(self) -> float:
+        return -1.0 if self.direction == "max" else 1.0
+
+    def _merge(self, d, entries):
+        best = self._best[d]
+        best.extend(entries)
+        best.sort(key=lambda pair: pair[0])
+        del best[self.k:]
+
+    def update(self, batch, hoi):
+        vals = getattr(hoi, self.measure)
+        b, d_count = vals.shape
+        if self._best is None:
+            self._best = [[] for _ in range(d_count)]
+        sign = self.sign
+        k_eff = min(self.k, b)
+        for d in range(d_count):
+            key = sign * vals[:, d]
+            thr = np.partition(key, k_eff - 1)[k_eff - 1]
+            new = []
+            for i in np.flatnonzero(key <= thr):
+                idx = batch.row_indices(int(i))
+                e = TopEntry(indices=idx, order=len(idx), value=float(vals[i, d]),
+                             tc=float(hoi.tc[i, d]), dtc=float(hoi.dtc[i, d]),
+                             o=float(hoi.o[i, d]), s=float(hoi.s[i, d]))
+                new.append(((sign * e.value, idx), e))
+            self._merge(d, new)
+
+    def finalize(self):
+        if self._best is None:
+            return []
+        return [[e for _, e in per] for per in self._best]
+
+
+class Histogram(Reducer):
+    """Clipped fixed-range histogram of one measure per dataset (ref:scanner.py:108-137)."""
+
+    def __init__(self, measure: str, bins: int, lo: float, hi: float):
+        if measure not in MEASURES:
+            raise InvalidData(f"measure must be one of {MEASURES}, got {measure!r}")
+        if bins < 1:
+            raise InvalidData(f"bins must be >= 1, got {bins}")
+        if not lo < hi:
+            raise InvalidData(f"need lo < hi, got [{lo}, {hi}]")
+        self.measure = measure
+        self.edges = np.linspace(lo, hi, bins + 1)
+        self._counts = None
+
+    def update(self, batch, hoi):
+        vals = getattr(hoi, self.measure)
+        if self._counts is None:
+            self._counts = np.zeros((vals.shape[1], len(self.edges) - 1), dtype=np.int64)
+        lo, hi = self.edges[0], self.edges[-1]
+        for d in range(vals.shape[1]):
+            self._counts[d] += np.histogram(np.clip(vals[:, d], lo, hi), bins=self.edges)[0]
+
+    def finalize(self):
+        return self.edges, self._counts
+
+
+class Callback(Reducer):
+    """Calls fn(batch, hoi) per batch in enumeration order (ref:scanner.py:140-154)."""
+
+    def __init__(self, fn):
+        if not callable(fn):
+            raise InvalidData("Callback needs a callable")
+        self.fn = fn
+        self._results = []
+
+    def update(self, batch, hoi):
+        self._results.append(self.fn(batch, hoi))
+
+    def finalize(self):
+        return self._results
+
+
+FEATURE_NAMES = (
+    "tc_max", "tc_min", "tc_mean", "tc_whole",
+    "dtc_max", "dtc_min", "dtc_mean", "dtc_whole",
+    "o_max", "o_min", "o_mean", "o_whole",
+    "s_max", "s_min", "s_mean", "s_whole",
+    "mi_mean", "mi_std",
+    "o_max_order_norm", "o_min_order_norm",
+    "prop_synergistic",
+)
+
+
+@dataclass(frozen=True)
+class FeatureVector:
+    """The 21-feature fingerprint of one dataset (ref:scanner.py:168-202)."""
+
+    tc_max: float
+    tc_min: float
+    tc_mean: float
+    tc_whole: float
+    dtc_max: float
+    dtc_min: float
+    dtc_mean: float
+    dtc_whole: float
+    o_max: float
+    o_min: float
+    o_mean: float
+    o_whole: float
+    s_max: float
+    s_min: float
+    s_mean: float
+    s_whole: float
+    mi_mean: float
+    mi_std: float
+    o_max_order_norm: float
+    o_min_order_norm: float
+    prop_synergistic: float
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name in FEATURE_NAMES}
+
+
+class FeatureAccumulator(Reducer):
+    """Streaming 21-feature accumulator over orders 2..N (ref:scanner.py:205-287)."""
+
+    def __init__(self, n_variables: int):
+        self.n = int(n_variables)
+        self._d = None
+
+    def _init_state(self, d_count):
+        self._d = d_count
+        self._sums = np.zeros((d_count, 4))
+        self._maxs = np.full((d_count, 4), -np.inf)
+        self._mins = np.full((d_count, 4), np.inf)
+        self._count = 0
+        self._o_max_order = np.zeros(d_count, dtype=np.int64)
+        self._o_min_order = np.zeros(d_count, dtype=np.int64)
+        self._syn = np.zeros(d_count, dtype=np.int64)
+        self._mi_sum = np.zeros(d_count)
+        self._mi_sumsq = np.zeros(d_count)
+        self._mi_count = 0
+        self._whole = np.full((d_count, 4), np.nan)
+
+    def update(self, batch, hoi):
+        vals = np.stack([hoi.tc, hoi.dtc, hoi.o, hoi.s], axis=-1)
+        if self._d is None:
+            self._init_state(vals.shape[1])
+        orders = hoi.order
+        pair = orders == 2
+        if pair.any():
+            mi = hoi.tc[pair]
+            self._mi_sum += mi.sum(axis=0)
+            self._mi_sumsq += (mi * mi).sum(axis=0)
+            self._mi_count += int(pair.sum())
+        rows = orders >= 3
+        if rows.any():
+            v = vals[rows]
+            o_col = hoi.o[rows]
+            row_orders = orders[rows]
+            for d in range(self._d):
+                i_max = int(np.argmax(o_col[:, d]))
+                if o_col[i_max, d] > self._maxs[d, 2]:
+                    self._o_max_order[d] = row_orders[i_max]
+                i_min = int(np.argmin(o_col[:, d]))
+                if o_col[i_min, d] < self._mins[d, 2]:
+                    self._o_min_order[d] = row_orders[i_min]
+            np.maximum(self._maxs, v.max(axis=0), out=self._maxs)
+            np.minimum(self._mins, v.min(axis=0), out=self._mins)
+            self._sums += v.sum(axis=0)
+            self._count += v.shape[0]
+            self._syn += (o_col < 0.0).sum(axis=0)
+            whole = np.flatnonzero(row_orders == self.n)
+            if whole.size:
+                self._whole = v[whole[0]]
+
+    def finalize(self):
+        if self._d is None or self._count == 0 or self._mi_count == 0:
+            raise InvalidData("feature accumulation needs orders 2..N")
+        if np.isnan(self._whole).any():
+            raise InvalidData("feature accumulation never saw the order-N row")
+        out = []
+        for d in range(self._d):
+            means = self._sums[d] / self._count
+            mi_mean = self._mi_sum[d] / self._mi_count
+            mi_var = max(self._mi_sumsq[d] / self._mi_count - mi_mean * mi_mean, 0.0)
+            kw = {}
+            for m_i, m in enumerate(MEASURES):
+                kw[f"{m}_max"] = float(self._maxs[d, m_i])
+                kw[f"{m}_min"] = float(self._mins[d, m_i])
+                kw[f"{m}_mean"] = float(means[m_i])
+                kw[f"{m}_whole"] = float(self._whole[d, m_i])
+            kw["mi_mean"] = float(mi_mean)
+            kw["mi_std"] = float(np.sqrt(mi_var))
+            kw["o_max_order_norm"] = float(self._o_max_order[d] / self.n)
+            kw["o_min_order_norm"] = float(self._o_min_order[d] / self.n)
+            kw["prop_synergistic"] = float(self._syn[d] / self._count)
+            out.append(FeatureVector(**kw))
+        return out
+
+
+# ------------------------------------------------------------- device scan --
+
+class DeviceScan:
+    """Full output of an exhaustive scan resident on the device.
+
+    ``out`` is a (4, rows, D) float64 tensor (tc, dtc, o, s) for the global
+    ranks [g_begin, g_end) of orders min_order..max_order."""
+
+    def __init__(self, out, n, min_order, max_order, g_begin, g_end):
+        self.out, self.n = out, n
+        self.min_order, self.max_order = min_order, max_order
+        self.g_begin, self.g_end = g_begin, g_end
+
+    def offsets(self):
+        off, acc = {}, 0
+        for k in range(self.min_order, self.max_order + 1):
+            off[k] = acc
+            acc += math.comb(self.n, k)
+        return off
+
+
+class _ScanCtx:
+    def __init__(self, covs, lo, hi, bias_correct, engine=0):
+        self.st = device_covs(covs)
+        self.torch = self.st.torch
+        self.n, self.d = self.st.n, self.st.d
+        self.lo, self.hi = lo, hi
+        self.eta = self.st.eta(hi) if bias_correct else None
+        self.engine = engine
+        self.ws = None
+        self.ws_bytes = ctypes.c_size_t(0)
+
+    def full(self, g0, g1, out=None):
+        torch, lib = self.torch, nat.lib()
+        rows = g1 - g0
+        if out is None:
+            out = torch.empty((4, rows, self.d), dtype=torch.float64, device="cuda")
+        cnt, coords = _err_buffers(torch)
+        kst = 0 if self.eta is None else self.eta.shape[1]
+        args = (self.st.corr.data_ptr(), self.st.sdiag.data_ptr(), nat.ptr(self.eta), kst,
+                self.n, self.d, self.lo, self.hi, g0, g1, self.engine)
+        if self.ws is None:
+            need = ctypes.c_size_t(0)
+            nat.check(lib.hoi_scan_full(*args, None, None, None, 0, None, ctypes.byref(need), None),
+                      "scan_full")
+            self.ws = torch.empty(max(int(need.value), 8), dtype=torch.uint8, device="cuda")
+            self.ws_bytes = ctypes.c_size_t(self.ws.numel())
+        nat.check(lib.hoi_scan_full(*args, out.data_ptr(), cnt.data_ptr(), coords.data_ptr(),
+                                    ERR_CAP, self.ws.data_ptr(), ctypes.byref(self.ws_bytes),
+                                    nat.stream_handle(torch)), "scan_full")
+        return out, cnt, coords
+
+
+def scan_device(covs: CovSet, min_order: int, max_order: int, *, bias_correct: bool = False,
+                g_begin: int = 0, g_end: int | None = None, engine: int = 0,
+                out=None) -> DeviceScan:
+    """Exhaustive full-output scan kept on the device (extension of the
+    reference API: the equivalent of collecting every batch of
+    ``scan(..., Callback(...))`` without leaving HBM)."""
+    n = covs.n_variables
+    total = count_nplets(n, min_order, max_order)
+    if n > 64:
+        raise InvalidOrderRange("scan_device supports N <= 64")
+    g_end = total if g_end is None else g_end
+    ctx = _ScanCtx(covs, min_order, max_order, bias_correct, engine)
+    o, cnt, coords = ctx.full(g_begin, g_end, out)
+    _raise_not_pd(cnt, coords)
+    return DeviceScan(o, n, min_order, max_order, g_begin, g_end)
+
+
+def _batch_bounds(n, lo, hi, batch_size):
+    """The reference's batch sequence as (g_start, g_stop, order)."""
+    off = 0
+    for k in range(lo, hi + 1):
+        c = math.comb(n, k)
+        for s in range(0, c, batch_size):
+            yield off + s, off + min(s + batch_size, c), k
+        off += c
+
+
+def _chunk_rows(d: int, torch) -> int:
+    free, _ = torch.cuda.mem_get_info()
+    budget = min(int(free * 0.4), 8 << 30)
+    return max(1 << 16, budget // (4 * 8 * d + 8 * 64))
+
+
+def _unrank_list(n, lo, hi, ranks):
+    """Index tuples of the given global ranks (device unranking)."""
+    torch = nat.torch_cuda()
+    r = torch.as_tensor(np.asarray(ranks, dtype=np.int64), device="cuda")
+    m = r.numel()
+    if m == 0:
+        return []
+    idx = torch.empty((m, hi), dtype=torch.int32, device="cuda")
+    orders = torch.empty(m, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib().hoi_unrank_list(n, lo, hi, r.data_ptr(), m, idx.data_ptr(),
+                                        orders.data_ptr(), nat.stream_handle(torch)), "unrank_list")
+    hi_idx, ho = idx.cpu().numpy(), orders.cpu().numpy()
+    return [tuple(int(v) for v in hi_idx[i, :ho[i]]) for i in range(m)]
+
+
+def _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0):
+    torch = ctx.torch
+    from .nplet_engine import unrank_device
+    bounds = list(_batch_bounds(ctx.n, ctx.lo, ctx.hi, batch_size))
+    per_chunk = _chunk_rows(ctx.d, torch)
+    i, seen, nb = 0, 0, 0
+    while i < len(bounds):
+        j, rows = i, 0
+        while j < len(bounds) and (rows == 0 or rows + bounds[j][1] - bounds[j][0] <= per_chunk):
+            rows += bounds[j][1] - bounds[j][0]
+            j += 1
+        g0, g1 = bounds[i][0], bounds[j - 1][1]
+        out, cnt, coords = ctx.full(g0, g1)
+        try:
+            _raise_not_pd(cnt, coords)
+        except Exception as e:  # map to the reference's per-batch coordinates
+            if getattr(e, "coords", None):
+                r0 = e.coords[0][0]
+                bsel = next(b for b in bounds[i:j] if b[0] <= g0 + r0 < b[1])
+                e.coords = [(g0 + r - bsel[0], d) for r, d in e.coords if bsel[0] <= g0 + r < bsel[1]]
+            raise
+        idx, _ = unrank_device(ctx.n, ctx.lo, ctx.hi, g0, g1 - g0)
+        host = out.cpu().numpy()
+        hidx = idx.cpu().numpy().astype(np.int64)
+        for (a, b, k) in bounds[i:j]:
+            ra, rb = a - g0, b - g0
+            batch = NpletBatch(ctx.n, indices=hidx[ra:rb, :k], check_unique=False)
+            hoi = HoiBatch(tc=host[0, ra:rb], dtc=host[1, ra:rb], o=host[2, ra:rb],
+                           s=host[3, ra:rb], order=np.full(rb - ra, k, dtype=np.int64))
+            reducer.update(batch, hoi)
+            nb += 1
+            seen += rb - ra
+            if progress is not None:
+                progress({"batches": nb, "nplets": seen, "total": total, "order": int(k),
+                          "elapsed": time.perf_counter() - t0})
+        i = j
+
+
+def _emit_progress(progress, n, lo, hi, batch_size, total, t0):
+    if progress is None:
+        return
+    seen = 0
+    for i, (a, b, k) in enumerate(_batch_bounds(n, lo, hi, batch_size)):
+        seen += b - a
+        progress({"batches": i + 1, "nplets": seen, "total": total, "order": int(k),
+                  "elapsed": time.perf_counter() - t0})
+
+
+def _topk_plane(ctx, reducer, out, g0, m_idx):
+    """Merge one device chunk into the running per-dataset TopK lists."""
+    torch = ctx.torch
+    lib = nat.lib()
+    rows = out.shape[1]
+    sign = reducer.sign
+    if reducer._best is None:
+        reducer._best = [[] for _ in range(ctx.d)]
+    plane = out[m_idx]
+    cap = max(1 << 20, 64 * reducer.k)
+    cand = torch.empty(cap, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    th = torch.empty(1, dtype=torch.float64, device="cuda")
+    for d in range(ctx.d):
+        best = reducer._best[d]
+        run = best[-1][0][0] if len(best) >= reducer.k else math.inf
+        if rows <= cap // 2:
+            taus = [math.inf]
+        else:
+            samp_n = min(rows, 1 << 15)
+            pos = torch.linspace(0, rows - 1, samp_n, device="cuda").round().long()
+            samp = np.sort(sign * plane[pos, d].cpu().numpy())
+            taus = []
+            for mult in (2, 8, 32, 128):
+                q = min(samp_n - 1, int(math.ceil(reducer.k * samp_n / rows * mult)) + 16)
+                taus.append(float(samp[q]))
+            taus.append(math.inf)
+        for tau in taus:
+            tau = min(tau, run)
+            th.fill_(tau)
+            cnt.zero_()
+            nat.check(lib.hoi_topk_filter(plane.data_ptr(), rows, ctx.d, d, sign, th.data_ptr(),
+                                          cand.data_ptr(), cnt.data_ptr(), cap,
+                                          nat.stream_handle(torch)), "topk_filter")
+            c = int(cnt.item())
+            if c > cap:
+                raise NotImplementedError(
+                    f"TopK: {c} candidates tie within the selection threshold "
+                    f"(more than the {cap}-row candidate buffer)")
+            have = sum(1 for kk, _ in best if kk[0] <= tau)
+            if c + have >= reducer.k or tau == run or math.isinf(tau):
+                break
+        pos = cand[:c]
+        vals = out[:, pos, d].cpu().numpy()            # (4, c)
+        tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, (pos + g0).cpu().numpy()) if c else []
+        mv = vals[m_idx]
+        new = []
+        for i in range(c):
+            e = TopEntry(indices=tuples[i], order=len(tuples[i]), value=float(mv[i]),
+                         tc=float(vals[0, i]), dtc=float(vals[1, i]), o=float(vals[2, i]),
+                         s=float(vals[3, i]))
+            new.append(((sign * e.value, e.indices), e))
+        reducer._merge(d, new)
+
+
+def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):
+    torch = ctx.torch
+    per_chunk = _chunk_rows(ctx.d, torch)
+    hist_counts = None
+    if isinstance(reducer, Histogram):
+        edges = torch.from_numpy(reducer.edges).cuda()
+        hist_counts = torch.zeros((ctx.d, len(reducer.edges) - 1), dtype=torch.int64, device="cuda")
+    m_idx = MEASURES.index(reducer.measure)
+    g0 = 0
+    while g0 < total:
+        g1 = min(total, g0 + per_chunk)
+        out, cnt, coords = ctx.full(g0, g1)
+        _raise_not_pd(cnt, coords)
+        if hist_counts is not None:
+            nat.check(nat.lib().hoi_histogram(
+                out[m_idx].data_ptr(), g1 - g0, ctx.d, len(reducer.edges) - 1,
+                float(reducer.edges[0]), float(reducer.edges[-1]), edges.data_ptr(),
+                hist_counts.data_ptr(), nat.stream_handle(torch)), "histogram")
+        else:
+            _topk_plane(ctx, reducer, out, g0, m_idx)
+        g0 = g1
+    if hist_counts is not None:
+        c = hist_counts.cpu().numpy()
+        reducer._counts = c if reducer._counts is None else reducer._counts + c
+    _emit_progress(progress, ctx.n, ctx.lo, ctx.hi, batch_size, total, t0)
+
+
+def scan(covs: CovSet, min_order: int, max_order: int, reducer: Reducer, *,
+         batch_size: int = 10000, bias_correct: bool = False, workers: int = 1, progress=None):
+    """Visit every n-plet with order in [min_order, max_order] once
+    (ref:scanner.py:308-365); returns reducer.finalize()."""
+    if not isinstance(reducer, Reducer):
+        raise InvalidData("reducer must be a Reducer instance")
+    n = covs.n_variables
+    total = count_nplets(n, min_order, max_order)
+    if workers < 1:
+        raise InvalidData(f"workers must be >= 1, got {workers}")
+    if batch_size < 1:
+        raise InvalidData(f"batch_size must be >= 1, got {batch_size}")
+    t0 = time.perf_counter()
+    if n > 64:
+        # beyond the unranking table: host-enumerated batches, device math
+        from .nplet_engine import enumerate_order  # noqa: F401  (N <= 64 only)
+        import itertools
+        seen = 0
+        nb = 0
+        for k in range(min_order, max_order + 1):
+            it = itertools.combinations(range(n), k)
+            while True:
+                flat = np.fromiter(itertools.chain.from_iterable(itertools.islice(it, batch_size)),
+                                   dtype=np.int64)
+                if flat.size == 0:
+                    break
+                batch = NpletBatch(n, indices=flat.reshape(-1, k), check_unique=False)
+                reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct=bias_correct))
+                nb += 1
+                seen += batch.batch_size
+                if progress is not None:
+                    progress({"batches": nb, "nplets": seen, "total": total, "order": k,
+                              "elapsed": time.perf_counter() - t0})
+        return reducer.finalize()
+    ctx = _ScanCtx(covs, min_order, max_order, bias_correct)
+    if type(reducer) in (TopK, Histogram):
+        _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0)
+    else:
+        _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0)
+    return reducer.finalize()
+
+
+def extract_features(covs: CovSet, *, bias_correct: bool = False, limit: int = 20,
+                     batch_size: int = 10000, workers: int = 1, progress=None):
+    """21 features per dataset from one scan of orders 2..N (ref:scanner.py:368-387)."""
+    n = covs.n_variables
+    if n > limit:
+        raise ExhaustiveLimitExceeded(
+            f"N={n} exceeds the exhaustive feature limit ({limit}); use greedy or annealing search")
+    if n < 3:
+        raise InvalidOrderRange(f"feature extraction needs N >= 3, got {n}")
+    return scan(covs, 2, n, FeatureAccumulator(n), batch_size=batch_size,
+                bias_correct=bias_correct, workers=workers, progress=progress)

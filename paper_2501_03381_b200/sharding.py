@@ -1,0 +1,124 @@
+"""Multi-GPU sharding of the n-plet rank space (one process per GPU).
+
+Every (n-plet, dataset) is independent, so the global order-major
+lexicographic rank space [0, total) is cut into contiguous ranges, one per
+rank, balanced by cost.  Nothing is exchanged while computing; the only
+collectives are the final merges:
+
+* full output -- shards are contiguous slices of the global order, so
+  concatenating them in rank order is bit-identical to a one-GPU scan;
+* TopK -- every rank's local top-k (value, index tuple, measures) is
+  all-gathered and merged with the reference's (sign*value, tuple) key;
+* Histogram -- counts are summed (all-reduce).
+
+Collectives go through torch.distributed (NCCL over NVLink on the GPU box,
+gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def nplet_flops(k: int) -> float:
+    """Algorithmic FP64 flops per (n-plet, dataset) of order k for the
+    per-n-plet engine: (k^3-k)/3 (LDL^T) + (k^3-k)/3 (triangular inverse)
+    + k(k+1) (inverse-diagonal column norms); one FMA = 2 flops."""
+    return 2.0 * (k ** 3 - k) / 3.0 + k * (k + 1)
+
+
+def order_offsets(n: int, lo: int, hi: int):
+    off, acc = [], 0
+    for k in range(lo, hi + 1):
+        off.append(acc)
+        acc += math.comb(n, k)
+    return off, acc
+
+
+def rank_ranges(n: int, lo: int, hi: int, world: int, weight: str = "count"):
+    """Contiguous [g0, g1) per rank with (approximately) equal cost.
+
+    weight="count": equal n-plet counts (the lattice engine's cost is flat
+    per n-plet); weight="flops": equal sum of nplet_flops(k) (the per-n-plet
+    engine's cost grows as k^3).  Cuts may fall inside an order."""
+    offs, total = order_offsets(n, lo, hi)
+    if weight == "count":
+        cuts = [total * r // world for r in range(world + 1)]
+        return [(cuts[r], cuts[r + 1]) for r in range(world)]
+    ks = list(range(lo, hi + 1))
+    cost = [math.comb(n, k) * nplet_flops(k) for k in ks]
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    bounds = [0]
+    for r in range(1, world):
+        target = cum[-1] * r / world
+        i = int(np.searchsorted(cum, target, side="right")) - 1
+        i = min(i, len(ks) - 1)
+        within = (target - cum[i]) / nplet_flops(ks[i])
+        g = offs[i] + int(round(within))
+        bounds.append(max(bounds[-1], min(g, total)))
+    bounds.append(total)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def merge_topk(partials, k: int):
+    """Merge per-rank TopK partial lists (each a list over datasets of
+    ((key_value, index_tuple), entry) pairs) deterministically."""
+    d_count = max(len(p) for p in partials)
+    merged = []
+    for d in range(d_count):
+        pool = [pair for p in partials for pair in (p[d] if d < len(p) else [])]
+        pool.sort(key=lambda pair: pair[0])
+        merged.append(pool[:k])
+    return merged
+
+
+def allgather_objects(obj, group=None):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def allreduce_counts(counts: np.ndarray, group=None, device="cpu") -> np.ndarray:
+    import torch
+    import torch.distributed as dist
+    t = torch.as_tensor(counts, dtype=torch.int64, device=device).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t.cpu().numpy()
+
+
+def scan_sharded(covs, lo, hi, reducer, *, bias_correct=False, group=None):
+    """Run this rank's slice of an exhaustive scan on its GPU and merge the
+    TopK / Histogram result across ranks (all ranks return the same value)."""
+    import torch.distributed as dist
+
+    from .nplet_engine import _raise_not_pd
+    from .scanner import Histogram, MEASURES, TopK, _ScanCtx, _topk_plane
+    import torch
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = covs.n_variables
+    weight = "count" if n <= 34 else "flops"
+    g0, g1 = rank_ranges(n, lo, hi, world, weight)[rank]
+    ctx = _ScanCtx(covs, lo, hi, bias_correct)
+    out, cnt, coords = ctx.full(g0, g1)
+    _raise_not_pd(cnt, coords)
+    m = MEASURES.index(reducer.measure)
+    if type(reducer) is TopK:
+        _topk_plane(ctx, reducer, out, g0, m)
+        parts = allgather_objects(reducer._best, group)
+        reducer._best = merge_topk(parts, reducer.k)
+    elif type(reducer) is Histogram:
+        from . import _native as nat
+        edges = torch.from_numpy(reducer.edges).cuda()
+        c = torch.zeros((ctx.d, len(reducer.edges) - 1), dtype=torch.int64, device="cuda")
+        nat.check(nat.lib().hoi_histogram(out[m].data_ptr(), g1 - g0, ctx.d, c.shape[1],
+                                          float(reducer.edges[0]), float(reducer.edges[-1]),
+                                          edges.data_ptr(), c.data_ptr(),
+                                          nat.stream_handle(torch)), "histogram")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
+        reducer._counts = c.cpu().numpy()
+    else:
+        raise TypeError("scan_sharded supports TopK and Histogram reducers")
+    return reducer.finalize()

@@ -1,0 +1,324 @@
+"""CUDA path vs the reference's golden vectors and the CPU oracle.
+
+Tolerances: measures rtol 1e-9 / atol 1e-11 (the reference's own
+acceptance tolerance, ref tests/test_acceptance.py:81 and the north_star's
+FP64 bound); covariance rtol 1e-12; ranks, copula values, enumeration
+and n-plet order bit-exact.
+"""
+
+import itertools
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_03381_b200 as hoi
+from paper_2501_03381_b200 import _build, _native, workloads
+from paper_2501_03381_b200.nplet_engine import _batched_logdet_invdiag, unrank_device
+
+pytestmark = pytest.mark.gpu
+RTOL, ATOL = 1e-9, 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    _build.build()
+    _native.load()
+    yield
+
+
+def collect(covs, lo, hi, bias=False, batch_size=10000):
+    rows, vals = [], []
+
+    def keep(batch, h):
+        rows.extend(batch.row_indices(i) for i in range(batch.batch_size))
+        vals.append(np.stack([h.tc, h.dtc, h.o, h.s]))
+
+    hoi.scan(covs, lo, hi, hoi.Callback(keep), batch_size=batch_size, bias_correct=bias)
+    return rows, np.concatenate(vals, axis=1)
+
+
+# ------------------------------------------------------------ copula ----
+
+def test_rank_copula_bit_exact(golden):
+    g = golden.npz("copula")
+    np.testing.assert_array_equal(hoi.rank_columns(g["x"]), g["ranks"])
+    np.testing.assert_array_equal(hoi.copula_transform(hoi.DataMatrix(g["x"])).values, g["z"])
+    np.testing.assert_array_equal(hoi.rank_columns(g["tie"])[:, 0], [3, 1, 4, 2])
+    cov = hoi.estimate_covariance(hoi.copula_transform(g["x"]))
+    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12)
+    np.testing.assert_array_equal(cov.sigma, cov.sigma.T)
+    assert cov.n_samples_used == 40
+
+
+def test_copula_multichunk_with_ties(golden):
+    import hashlib
+    g = golden.npz("cfg3")
+    x = workloads.cfg3()                       # T = 10,000 > one 8192-row chunk, 13 ties
+    r = hoi.rank_columns(x)
+    assert hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest() == str(g["ranks_sha"])
+    cov = hoi.estimate_covariance(hoi.copula_transform(x))
+    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12)
+    np.testing.assert_array_equal(cov.sigma, cov.sigma.T)
+
+
+def test_copula_monotone_invariance_and_cfg4(golden):
+    x = workloads.cfg4()
+    z = hoi.copula_transform(x).values
+    np.testing.assert_array_equal(hoi.copula_transform(np.exp(x / 10.0)).values, z)
+    cov = hoi.estimate_covariance(hoi.copula_transform(x))
+    np.testing.assert_allclose(cov.sigma, golden.npz("cfg4")["cov"], rtol=1e-12)
+
+
+# -------------------------------------------------------- enumeration ---
+
+def test_unranking_is_itertools_order():
+    for n, lo, hi in [(12, 1, 12), (7, 3, 3), (20, 18, 20)]:
+        total = hoi.count_nplets(n, lo, hi)
+        idx, orders = unrank_device(n, lo, hi, 0, total)
+        idx, orders = idx.cpu().numpy(), orders.cpu().numpy()
+        want = [c for k in range(lo, hi + 1) for c in itertools.combinations(range(n), k)]
+        got = [tuple(int(v) for v in idx[i, :orders[i]]) for i in range(total)]
+        assert got == want
+    # 64-variable edges (largest binomials in the table)
+    for k in (1, 2, 63, 64):
+        c = math.comb(64, k)
+        idx, _ = unrank_device(64, k, k, c - 1, 1)
+        assert tuple(idx[0].tolist()) == tuple(range(64 - k, 64))
+
+
+def test_enumerate_order_batches():
+    got = []
+    for batch in hoi.enumerate_order(7, 3, batch_size=4):
+        assert batch.batch_size <= 4
+        got.extend(batch.row_indices(i) for i in range(batch.batch_size))
+    assert got == list(itertools.combinations(range(7), 3))
+
+
+# ------------------------------------------------------ full scans ------
+
+@pytest.mark.parametrize("batch_size", [7, 10000])
+def test_cfg1_full_scan(golden, batch_size):
+    g = golden.npz("cfg1")
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(g["x"]))])
+    rows, vals = collect(covs, 3, 10, batch_size=batch_size)
+    assert rows == [c for k in range(3, 11) for c in itertools.combinations(range(10), k)]
+    np.testing.assert_allclose(vals[:, :, 0], g["vals"], rtol=RTOL, atol=ATOL)
+    np.testing.assert_array_equal(vals[3], vals[0] + vals[1])      # s == tc + dtc exactly
+
+
+def test_cfg2_full_scan_with_bias(golden):
+    g = golden.npz("cfg2")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    _, vals = collect(covs, 3, 12, bias=True)
+    np.testing.assert_allclose(vals[:, :, 0], g["vals"], rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("cfg,lo,hi", [("cfg3", 3, 20), ("cfg4", 2, 30)])
+@pytest.mark.parametrize("bias", [False, True])
+def test_sampled_ranks_batched_and_scanned(golden, cfg, lo, hi, bias):
+    g = golden.npz(cfg)
+    key = "vals_bias" if bias else "vals"
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    rows = [tuple(int(v) for v in r if v >= 0) for r in g["idx"]]
+    by_k = {}
+    for i, t in enumerate(rows):
+        by_k.setdefault(len(t), []).append(i)
+    got = np.empty_like(g[key])
+    for k, sel in by_k.items():
+        h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(covs.n_variables,
+                                                       indices=np.array([rows[i] for i in sel])),
+                                  bias_correct=bias)
+        got[:, sel, :] = np.stack([h.tc, h.dtc, h.o, h.s])
+    np.testing.assert_allclose(got, g[key], rtol=RTOL, atol=ATOL)
+    if cfg == "cfg3":   # whole 1,048,365-row scan on the device, checked at the sampled ranks
+        dev = hoi.scan_device(covs, lo, hi, bias_correct=bias)
+        out = dev.out[:, torch.as_tensor(g["g"], device="cuda"), :].cpu().numpy()
+        np.testing.assert_allclose(out, g[key], rtol=RTOL, atol=ATOL)
+
+
+def test_cfg4_full_exhaustive_scan(golden):
+    """The headline configuration: all 1,073,741,793 n-plets of orders 2..30."""
+    g = golden.npz("cfg4")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    dev = hoi.scan_device(covs, 2, 30)
+    out = dev.out
+    assert out.shape == (4, hoi.count_nplets(30, 2, 30), 1)
+    sel = torch.as_tensor(g["g"], device="cuda")
+    np.testing.assert_allclose(out[:, sel, :].cpu().numpy(), g["vals"], rtol=RTOL, atol=ATOL)
+    # size-independent properties over every row
+    assert bool(torch.isfinite(out).all())
+    assert bool((out[3] == out[0] + out[1]).all())
+    n2 = math.comb(30, 2)
+    assert float(out[2, :n2].abs().max()) < 1e-12                # O = 0 at order 2
+    assert bool((out[0] >= -1e-12).all())                        # TC >= 0
+    del out, dev
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------- edges ----
+
+def test_identity_exact_zeros_and_closed_forms(golden):
+    e = golden.npz("edge")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(np.eye(6))])
+    for k in (2, 3, 4, 6):
+        idx = np.array(list(itertools.combinations(range(6), k)))
+        h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(6, indices=idx))
+        for m in (h.tc, h.dtc, h.o, h.s):
+            assert (m == 0.0).all()
+    for m in (2, 3, 4):
+        for kind, fn in (("r", hoi.r_system_cov), ("s", hoi.s_system_cov)):
+            cov = fn(m, 1.0)
+            h = hoi.compute_hoi_batch(hoi.CovSet([cov]),
+                                      hoi.NpletBatch(m + 1, indices=np.arange(m + 1)[None]))
+            np.testing.assert_allclose([h.tc[0, 0], h.dtc[0, 0], h.o[0, 0], h.s[0, 0]],
+                                       e[f"rs_{kind}{m}"], atol=1e-13)
+    r2 = e["rs_r2"]
+    assert r2[0] == pytest.approx(math.log(2.0), abs=1e-14)
+    assert r2[2] == pytest.approx(0.5 * math.log(4.0 / 3.0), abs=1e-14)
+
+
+def test_not_pd_coords_and_jitter(golden):
+    e = golden.npz("edge")
+    bad = np.array([[1.0, 2.0], [2.0, 1.0]])
+    with pytest.raises(hoi.NotPositiveDefinite) as err:
+        _batched_logdet_invdiag(np.stack([np.eye(2), bad])[:, None])
+    assert [list(c) for c in err.value.coords] == golden.meta["edge"]["npd_coords"]
+    ld, idg = _batched_logdet_invdiag((np.ones((3, 3)) + np.eye(3) * 1e-14)[None, None])
+    assert np.isfinite(ld).all()
+    np.testing.assert_allclose(ld, e["singular_ld"], rtol=1e-6)
+    # healthy matrices are unaffected by a failing neighbour (bit-identical)
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((8, 3))
+    good = (a.T @ a / 8 + 0.5 * np.eye(3))[None, None]
+    stack = np.concatenate([good, (np.ones((3, 3)) + np.eye(3) * 1e-14)[None, None]])
+    l1, i1 = _batched_logdet_invdiag(stack)
+    l0, i0 = _batched_logdet_invdiag(good)
+    assert l1[0, 0] == l0[0, 0]
+    np.testing.assert_array_equal(i1[0, 0], i0[0, 0])
+
+
+def test_logdet_invdiag_vs_slogdet():
+    rng = np.random.default_rng(2)
+    mats = np.empty((4, 3, 5, 5))
+    for b in range(4):
+        for d in range(3):
+            a = rng.standard_normal((8, 5))
+            mats[b, d] = a.T @ a / 8 + 0.3 * np.eye(5)
+    ld, idg = _batched_logdet_invdiag(mats)
+    for b in range(4):
+        for d in range(3):
+            assert ld[b, d] == pytest.approx(np.linalg.slogdet(mats[b, d])[1], rel=1e-10)
+            np.testing.assert_allclose(idg[b, d], np.diag(np.linalg.inv(mats[b, d])), rtol=1e-10)
+
+
+def test_mixed_masks_and_terms(golden):
+    e = golden.npz("edge")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(e["mix_sigma"])])
+    batch = hoi.NpletBatch(15, masks=e["mix_masks"])
+    h = hoi.compute_hoi_batch(covs, batch)
+    np.testing.assert_allclose(np.stack([h.tc, h.dtc, h.o, h.s]), e["mix_vals"], rtol=RTOL,
+                               atol=ATOL)
+    t = hoi.entropy_terms(covs, batch)
+    np.testing.assert_allclose(t.h_joint, e["mix_hj"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(t.h_singles, e["mix_hs"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(t.h_leave_one_out, e["mix_hl"], rtol=1e-12, atol=1e-12)
+    cs2 = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=60) for s in e["t2_sig"]])
+    b2 = hoi.NpletBatch(6, indices=e["t2_idx"])
+    t2 = hoi.entropy_terms(cs2, b2, bias_correct=True)
+    np.testing.assert_allclose(t2.h_joint, e["t2_hj"], rtol=1e-12)
+    np.testing.assert_allclose(t2.h_singles, e["t2_hs"], rtol=1e-12)
+    np.testing.assert_allclose(t2.h_leave_one_out, e["t2_hl"], rtol=1e-12)
+    h2 = hoi.compute_hoi_batch(cs2, b2, bias_correct=True)
+    np.testing.assert_allclose(np.stack([h2.tc, h2.dtc, h2.o, h2.s]), e["t2_vals"], rtol=RTOL,
+                               atol=ATOL)
+
+
+# ----------------------------------------------------------- reducers ---
+
+def _entries(lst):
+    return [[list(e.indices), e.value, e.tc, e.dtc, e.o, e.s] for e in lst]
+
+
+def test_topk_and_histogram_on_toy_covsets(golden):
+    red = golden.meta["reducers"]
+    sig = {k: np.array(v) for k, v in golden.meta["toy_sigmas"].items()}
+    t1 = hoi.CovSet([hoi.CovarianceMatrix(sig["t1"][0])])
+    for direction in ("max", "min"):
+        got = _entries(hoi.scan(t1, 3, 5, hoi.TopK("o", direction, 7))[0])
+        want = red[f"top_o_{direction}"]
+        assert [g[0] for g in got] == [w[0] for w in want]
+        np.testing.assert_allclose([g[1:] for g in got], [w[1:] for w in want], rtol=RTOL, atol=ATOL)
+    t2 = hoi.CovSet([hoi.CovarianceMatrix(s) for s in sig["t2"]])
+    base = hoi.scan(t2, 3, 6, hoi.TopK("s", "max", 9))
+    for per_got, per_want in zip(base, red["top_s_max_d2"]):
+        assert [list(e.indices) for e in per_got] == [w[0] for w in per_want]
+    for bs, w in [(1, 1), (13, 1), (64, 3)]:
+        assert hoi.scan(t2, 3, 6, hoi.TopK("s", "max", 9), batch_size=bs, workers=w) == base
+    eye5 = hoi.CovSet([hoi.CovarianceMatrix(np.eye(5))])
+    got = hoi.scan(eye5, 3, 3, hoi.TopK("o", "max", 4), batch_size=2)
+    assert [list(e.indices) for e in got[0]] == red["top_tie"]
+    assert all(e.value == 0.0 for e in got[0])
+    t3 = hoi.CovSet([hoi.CovarianceMatrix(s) for s in sig["t3"]])
+    edges, c8 = hoi.scan(t3, 2, 4, hoi.Histogram("tc", 8, 0.0, 0.5))
+    assert c8.tolist() == red["hist_8"]
+    np.testing.assert_allclose(edges, np.linspace(0.0, 0.5, 9))
+    _, c2 = hoi.scan(t3, 2, 4, hoi.Histogram("tc", 2, 0.20, 0.21))
+    assert c2.tolist() == red["hist_2"]
+
+
+def test_cfg3_topk_histogram(golden):
+    g = golden.npz("cfg3")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    got = _entries(hoi.scan(covs, 3, 20, hoi.TopK("o", "min", 10))[0])
+    want = golden.meta["cfg3"]["top_o_min"]
+    assert [x[0] for x in got] == [w[0] for w in want]
+    np.testing.assert_allclose([x[1:] for x in got], [w[1:] for w in want], rtol=RTOL, atol=ATOL)
+    got = _entries(hoi.scan(covs, 3, 20, hoi.TopK("s", "max", 10), bias_correct=True)[0])
+    want = golden.meta["cfg3"]["top_s_max_bias"]
+    assert [x[0] for x in got] == [w[0] for w in want]
+    edges, counts = hoi.scan(covs, 3, 20, hoi.Histogram("o", 16, -0.5, 2.0))
+    np.testing.assert_array_equal(edges, g["hist_edges"])
+    assert int(np.abs(counts - g["hist_counts"]).sum()) <= 2   # edge-straddling rows only
+    assert counts.sum() == hoi.count_nplets(20, 3, 20)
+
+
+def test_features_and_callback_order(golden):
+    red = golden.meta["reducers"]
+    sig = {k: np.array(v) for k, v in golden.meta["toy_sigmas"].items()}
+    t7 = hoi.CovSet([hoi.CovarianceMatrix(s) for s in sig["t7"]])
+    feats = hoi.extract_features(t7)
+    for f, w in zip(feats, red["features_t7"]):
+        for name, v in w.items():
+            assert getattr(f, name) == pytest.approx(v, abs=1e-12), name
+    for f, w in zip(hoi.extract_features(hoi.CovSet([hoi.r_system_cov(3, 1.0)])), red["features_r3"]):
+        for name, v in w.items():
+            assert getattr(f, name) == pytest.approx(v, abs=1e-12), name
+    ident = hoi.extract_features(hoi.CovSet([hoi.CovarianceMatrix(np.eye(5))]))[0]
+    for name, v in ident.as_dict().items():
+        assert v == (3 / 5 if name.endswith("order_norm") else 0.0), name
+    ticks = []
+    hoi.scan(t7, 2, 4, hoi.TopK("o", "max", 1), batch_size=7, progress=ticks.append)
+    assert ticks[-1]["nplets"] == ticks[-1]["total"] == hoi.count_nplets(6, 2, 4)
+    assert [t["batches"] for t in ticks] == list(range(1, len(ticks) + 1))
+
+
+def test_cfg5_batched_large_system(oracle):
+    """D=16 datasets x N=400, order-10 n-plets (B x D pairing), vs the oracle."""
+    covs_np = []
+    for d in range(16):
+        x = workloads.cfg5_data(d)
+        covs_np.append(oracle.covariance(oracle.copula(x)))
+    sig = np.stack(covs_np)
+    idx = workloads.cfg5_nplets(b=2048)
+    covs = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=1200) for s in sig])
+    for bias in (False, True):
+        h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(400, indices=idx), bias_correct=bias)
+        tc, dtc, o, s, _ = oracle.hoi_batch(sig, [1200] * 16, idx=idx, bias=bias)
+        np.testing.assert_allclose(np.stack([h.tc, h.dtc, h.o, h.s]), np.stack([tc, dtc, o, s]),
+                                   rtol=RTOL, atol=ATOL)
+    # the device copula path agrees with the oracle on one dataset
+    cov0 = hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(0)))
+    np.testing.assert_allclose(cov0.sigma, sig[0], rtol=1e-12, atol=1e-15)
