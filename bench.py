@@ -193,6 +193,98 @@ def fp64_peak(torch, lib, nat):
     return best
 
 
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    return 6650.0, "fallback 6.65 TB/s from B200_PROFILING.md"
+
+
+def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
+    """Per-kernel CUDA-event timing of the two lattice phases on the
+    launching stream, repeated `steps` times; the dominant kernel is the
+    stencil/measures pass (HBM-bound: reads the 2^N log-det table, writes
+    4 x f64 per n-plet)."""
+    s = nat.stream_handle(torch)
+    ws, wsb = ctx.ws, ctx.ws.numel()
+    t_tab, t_mea = [], []
+    for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        nat.check(lib.hoi_lattice_table(ctx.st.corr.data_ptr(), N, 1, 0, ws.data_ptr(), wsb, s))
+        ev[1].record()
+        nat.check(lib.hoi_lattice_measures(ws.data_ptr(), N, 1, 0, None, 0, LO, HI, g0, g1,
+                                           out.data_ptr(), s))
+        ev[2].record()
+        torch.cuda.synchronize()
+        t_tab.append(ev[0].elapsed_time(ev[1]))
+        t_mea.append(ev[1].elapsed_time(ev[2]))
+    tm, tt = float(np.mean(t_mea)), float(np.mean(t_tab))
+    table_bytes = 8 * (1 << N)
+    alg = table_bytes + 32 * (g1 - g0)
+    peak, src = measured_peaks()
+    achieved = alg / (tm * 1e-3) / 1e9
+    traffic = None
+    tf = REPO / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("k_lattice_measures_bytes")
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "k_lattice_measures (leave-one-out stencil + TC/DTC/O/S epilogue)",
+            "peak_source": src,
+            "algorithmic_bytes_per_launch": alg,
+            "algorithmic_bytes_note": "8 B x 2^N log-det table read once + 32 B x n-plets written",
+            "kernel_ms": tm, "table_kernel_ms": tt,
+            "table_kernel_bytes": table_bytes,
+            "kernel_share_of_step": (tm + tt) / step_ms}
+
+
+def percell_roofline(torch, lib, nat, covs, g0, g1, step_ms):
+    """FP64 roofline of the per-n-plet engine (k_eval<K>: LDL^T + inverse
+    diagonal + epilogue) on the same workload: one CUDA-event-timed launch
+    per order segment on the launching stream."""
+    from paper_2501_03381_b200.scanner import _ScanCtx
+    from paper_2501_03381_b200.sharding import nplet_flops
+    ctx = _ScanCtx(covs, LO, HI, False, 1)
+    peak64 = fp64_peak(torch, lib, nat)
+    per = []
+    off = 0
+    for k in range(LO, HI + 1):
+        c = math.comb(N, k)
+        lo_, hi_ = max(off, g0), min(off + c, g1)
+        if lo_ < hi_:
+            seg = torch.empty((4, hi_ - lo_, 1), dtype=torch.float64, device="cuda")
+            ctx.full(lo_, hi_, seg)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            ctx.full(lo_, hi_, seg)
+            ev[1].record()
+            torch.cuda.synchronize()
+            per.append((k, hi_ - lo_, ev[0].elapsed_time(ev[1])))
+            del seg
+        off += c
+    flops = sum(nplet_flops(k) * cnt for k, cnt, _ in per)
+    kms = sum(t for _, _, t in per)
+    achieved = flops / (kms * 1e-3) / 1e12
+    traffic = None
+    tf = REPO / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("k_eval_bytes_per_step")
+    r = {"bound": "fp64", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
+         "frac": achieved / peak64, "traffic": traffic,
+         "kernel": "k_eval<K> (per-n-plet LDL^T + inverse diagonal + epilogue)",
+         "peak_source": "measured in this run: DFMA probe kernel (MEASURED_PEAKS.json "
+                        "has no FP64 entry)",
+         "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
+         "nplets_per_s": (g1 - g0) / (kms * 1e-3),
+         "per_order_ms": {int(k): round(t, 3) for k, _, t in per},
+         "hbm_out_bytes_per_step": 32 * (g1 - g0)}
+    if step_ms:
+        r["kernel_share_of_step"] = kms / step_ms
+    return r
+
+
 def b200_arm(a):
     import torch
     world, rank, local = dist_env()
@@ -246,41 +338,15 @@ def b200_arm(a):
     # the launching stream (engine 1: one launch per order segment)
     engine_used = ctx.engine
     roof = None
+    if rank == 0 and engine_used == 2:
+        roof = lattice_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     del out
     torch.cuda.empty_cache()
+    fp64 = None
     if rank == 0:
-        peak64 = fp64_peak(torch, lib, nat)
-        per = []
-        off = 0
-        for k in range(LO, HI + 1):
-            c = math.comb(N, k)
-            lo_, hi_ = max(off, g0), min(off + c, g1)
-            if lo_ < hi_:
-                seg = torch.empty((4, hi_ - lo_, 1), dtype=torch.float64, device="cuda")
-                ctx.full(lo_, hi_, seg)
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                ev[0].record()
-                ctx.full(lo_, hi_, seg)
-                ev[1].record()
-                torch.cuda.synchronize()
-                per.append((k, hi_ - lo_, ev[0].elapsed_time(ev[1])))
-                del seg
-            off += c
-        flops = sum(nplet_flops(k) * cnt for k, cnt, _ in per)
-        kms = sum(t for _, _, t in per)
-        achieved = flops / (kms * 1e-3) / 1e12
-        traffic = None
-        tf = REPO / "profiles" / "traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get("k_eval_bytes_per_step")
-        roof = {"bound": "fp64", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
-                "frac": achieved / peak64, "traffic": traffic,
-                "kernel": "k_eval<K> (per-n-plet LDL^T + inverse diagonal + epilogue)",
-                "peak_source": "measured in this run: DFMA probe kernel (MEASURED_PEAKS.json "
-                               "has no FP64 entry)",
-                "algorithmic_flops_per_step": flops, "kernel_ms_per_step": kms,
-                "kernel_share_of_step": kms / ms,
-                "hbm_out_bytes_per_step": 32 * (g1 - g0)}
+        fp64 = percell_roofline(torch, lib, nat, covs, g0, g1, ms if engine_used == 1 else None)
+        if engine_used == 1:
+            roof = fp64
 
     line = None
     if rank == 0:
@@ -297,6 +363,7 @@ def b200_arm(a):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "roofline": roof,
+            "per_nplet_engine": fp64,
         }
     torch.cuda.empty_cache()
 

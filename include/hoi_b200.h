@@ -45,7 +45,10 @@ enum {
   HOI_INSUFFICIENT_SAMPLES = 2, /* -> InsufficientSamples                   */
   HOI_NOT_PD = 3,               /* -> NotPositiveDefinite (see err buffers) */
   HOI_CUDA_ERROR = 4,
-  HOI_CAPACITY = 5              /* workspace / output too small             */
+  HOI_CAPACITY = 5,             /* workspace / output too small             */
+  HOI_FALLBACK = 6              /* lattice engine declined (matrix not PD):
+                                   rerun with engine 1, whose per-n-plet
+                                   jitter retry matches the reference      */
 };
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -161,6 +164,20 @@ int hoi_scan_full(const double *corr, const double *sdiag, const double *eta,
                   int32_t kmax, int64_t g_begin, int64_t g_end, int32_t engine,
                   double *out, int32_t *err_count, int64_t *err_coords,
                   int32_t err_cap, void *ws, size_t *ws_bytes, void *stream);
+
+/* The two phases of engine 2, exposed separately so a caller can time them
+ * or reuse one table across several rank ranges.  ws is the engine-2
+ * workspace of hoi_scan_full (query its size there).
+ *   hoi_lattice_table:    T[S] = log det R_S for all 2^N subsets of dataset d;
+ *   hoi_lattice_status:   synchronous; HOI_FALLBACK if a pivot was <= 0;
+ *   hoi_lattice_measures: stencil + measures for ranks [g_begin, g_end) of
+ *                         orders kmin..kmax into out (layout of hoi_scan_full). */
+int hoi_lattice_table(const double *corr, int32_t N, int32_t D, int32_t d, void *ws,
+                      size_t ws_bytes, void *stream);
+int hoi_lattice_status(void *ws, int32_t N, void *stream);
+int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, const double *eta,
+                         int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
+                         int64_t g_end, double *out, void *stream);
 
 /* ---------------------------------------------------------------------------
  * (5) Device reducers over a full-output plane (ref:scanner.py:50-137).

@@ -17,7 +17,7 @@ from .errors import (HoiError, InsufficientSamples, InvalidData, NotPositiveDefi
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhoib200.so"
 
-OK, INVALID_ARG, INSUFFICIENT_SAMPLES, NOT_PD, CUDA_ERROR, CAPACITY = range(6)
+OK, INVALID_ARG, INSUFFICIENT_SAMPLES, NOT_PD, CUDA_ERROR, CAPACITY, FALLBACK = range(7)
 
 _lock = threading.Lock()
 _lib = None
@@ -44,6 +44,10 @@ _SIGS = {
     "hoi_unrank_list": ([_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp], C.c_int),
     "hoi_scan_full": ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i32, _vp, _vp,
                        _vp, _i32, _vp, C.POINTER(_sz), _vp], C.c_int),
+    "hoi_lattice_table": ([_vp, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
+    "hoi_lattice_status": ([_vp, _i32, _vp], C.c_int),
+    "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,
+                              _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_histogram": ([_vp, _i64, _i32, _i32, _dbl, _dbl, _vp, _vp, _vp], C.c_int),
     "hoi_fp64_probe": ([_vp, _i64, _i32, _vp], C.c_int),

@@ -1,18 +1,475 @@
-// Engine 2: subset-lattice engine for exhaustive scans (placeholder until
-// the lattice kernels land; hoi_scan_full falls back to engine 1).
+// Engine 2: subset-lattice engine for exhaustive scans (12 <= N <= 32).
+//
+// In the correlation form every measure of an n-plet S of order k depends
+// on l(S) = log det R_S and on the leave-one-out log-determinants
+// l(S \ j), j in S (ref:nplet_engine.py:267-273: logdet(Sigma_-j) =
+// logdet Sigma + log (Sigma^-1)_jj):
+//   tc  = -l/2                        - k*eta1 + eta_k
+//   dtc = ((1-k) l + sum_j l(S\j))/2  + (k-1)*eta_k - k*eta_{k-1}
+//   o   = ((k-2) l - sum_j l(S\j))/2  - k*eta1 - (k-2)*eta_k + k*eta_{k-1}
+//   s   = tc + dtc
+// An exhaustive scan visits every subset, so every leave-one-out term is
+// itself the log-determinant of another visited subset.  The engine
+// therefore (phase 1) computes the table T[S] = l(S) for all 2^N subsets
+// with one Schur-complement elimination tree -- a handful of FMAs and ONE
+// log per subset instead of an O(k^3) factorisation -- and (phase 2)
+// streams the table through a hypercube stencil that sums the k
+// neighbours T[S \ j] and writes the four measures straight into the
+// order-major lexicographic output position.
+//
+// Table layout: variables 0..N-CB-1 form the block index ("prefix"
+// variables, bit j = variable j) and the last CB = 10 variables F form the
+// 1024-entry block (bit t = variable N-CB+t).  For a fixed prefix set P and
+// |Q| = q, the subsets P u Q (Q a q-subset of F) are CONTIGUOUS in the
+// reference's lexicographic order, so phase 2 writes C(10,q)-long
+// coalesced runs.
 #include "common.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace hoib {
+namespace {
+
+constexpr int CB = 10;            // suffix variables per block
+constexpr int BLK = 1 << CB;      // 1024 table entries per block
+constexpr int LANE_BITS = 5;      // F0..F4 -> lane, F5..F9 -> register recursion
+constexpr int MAXV = 32;          // max variables
+constexpr int MAXB = 6;           // prefix variables expanded inside one CTA
+constexpr double LN2 = 0.69314718055994530942;
+// Schur pivots of a correlation matrix lie in (0, 1]; a pivot below this
+// means R is (numerically) singular and the table would carry rounding
+// noise, so the engine declines and the per-n-plet engine (with the
+// reference's per-matrix jitter rule) takes the scan.
+constexpr double kMinPivot = 1e-12;
+
+__constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
+__constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
+__constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
+
+__device__ __forceinline__ void lp_mul(double &m, int &e, double x) {
+  m *= x;
+  double a = fabs(m);
+  if (a < 1e-150 || a > 1e150) {
+    int ex;
+    m = frexp(m, &ex);
+    e += ex;
+  }
+}
+
+__device__ __forceinline__ double lp_log(double m, int e) {
+  double l = log(m);
+  return e == 0 ? l : l + (double)e * LN2;
+}
+
+// Leaf recursion over the last R suffix variables held in registers as a
+// packed lower triangle.  Include/exclude variable 0 of the remainder; the
+// include branch takes the Schur complement.  2^R leaves, one log each.
+template <int R>
+struct Leaf {
+  static __device__ __forceinline__ void run(const double (&a)[R * (R + 1) / 2], double m, int e,
+                                             int bits, double *__restrict__ out, int lane,
+                                             int *bad) {
+    constexpr int R1 = R - 1;
+    double ex[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
+    // exclude variable (CB - R): remainder unchanged
+#pragma unroll
+    for (int i = 1; i < R; ++i)
+#pragma unroll
+      for (int l = 1; l <= i; ++l) ex[(i - 1) * i / 2 + (l - 1)] = a[i * (i + 1) / 2 + l];
+    Leaf<R1>::run(ex, m, e, bits, out, lane, bad);
+    // include: pivot a00, Schur complement of the rest
+    const double p = a[0];
+    if (!(p > kMinPivot)) *bad = 1;
+    const double rp = 1.0 / p;
+    double in[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
+#pragma unroll
+    for (int i = 1; i < R; ++i) {
+      const double ai = a[i * (i + 1) / 2] * rp;
+#pragma unroll
+      for (int l = 1; l <= i; ++l)
+        in[(i - 1) * i / 2 + (l - 1)] = fma(-ai, a[l * (l + 1) / 2], a[i * (i + 1) / 2 + l]);
+    }
+    double m2 = m;
+    int e2 = e;
+    lp_mul(m2, e2, p);
+    Leaf<R1>::run(in, m2, e2, bits | (1 << (CB - R)), out, lane, bad);
+  }
+};
+
+template <>
+struct Leaf<0> {
+  static __device__ __forceinline__ void run(const double (&)[1], double m, int e, int bits,
+                                             double *__restrict__ out, int lane, int *) {
+    // bits holds the F5..F9 pattern at bit positions 5..9
+    out[bits + lane] = lp_log(m, e);
+  }
+};
+
+// Phase 1: one CTA per pattern of the "fixed" prefix variables b..N-CB-1;
+// its 8 warps expand the 2^b patterns of prefix variables 0..b-1, and each
+// lane of a warp owns one pattern of F0..F4 and recurses over F5..F9.
+__global__ void __launch_bounds__(256)
+k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
+                double *__restrict__ table, int *__restrict__ flag) {
+  constexpr int MS = MAXV + 1;
+  __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
+  __shared__ double W[8][(MAXB + CB) * (MAXB + CB)];  // per-warp (b+CB)^2 work
+  __shared__ int vars[MAXV];
+  __shared__ int s_nfix;
+  __shared__ double s_m0;
+  __shared__ int s_e0;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nP = N - CB;
+  if (tid == 0) {
+    int nf = 0;
+    for (int j = b; j < nP; ++j)
+      if ((blockIdx.x >> (j - b)) & 1) vars[nf++] = j;
+    s_nfix = nf;
+    for (int j = 0; j < b; ++j) vars[nf + j] = j;
+    for (int t = 0; t < CB; ++t) vars[nf + b + t] = nP + t;
+    s_bad = 0;
+  }
+  __syncthreads();
+  const int nfix = s_nfix, m = nfix + b + CB;
+  for (int x = tid; x < m * m; x += blockDim.x) {
+    int i = x / m, l = x - i * m;
+    M[i * MS + l] = corr[((int64_t)vars[i] * N + vars[l]) * D + d];
+  }
+  __syncthreads();
+  // eliminate the fixed prefix variables (right-looking, full square)
+  double m0 = 1.0;
+  int e0 = 0;
+  for (int j = 0; j < nfix; ++j) {
+    const double p = M[j * MS + j];
+    if (tid == 0) {
+      if (!(p > kMinPivot)) s_bad = 1;
+      lp_mul(m0, e0, p);
+    }
+    const double rp = 1.0 / p;
+    const int r = m - j - 1;
+    for (int x = tid; x < r * r; x += blockDim.x) {
+      int i = j + 1 + x / r, l = j + 1 + x % r;
+      M[i * MS + l] = fma(-M[i * MS + j] * rp, M[j * MS + l], M[i * MS + l]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s_m0 = m0;
+    s_e0 = e0;
+  }
+  __syncthreads();
+  const int w = b + CB;                            // expansion size
+  double *Wm = W[warp];
+  const double *S0 = M + nfix * MS + nfix;
+  for (int u = warp; u < (1 << b); u += 8) {
+    for (int x = lane; x < w * w; x += 32) Wm[x] = S0[(x / w) * MS + (x % w)];
+    __syncwarp();
+    double mu = s_m0;
+    int eu = s_e0;
+    for (int j = 0; j < b; ++j) {
+      if (!((u >> j) & 1)) continue;               // warp-uniform
+      const double p = Wm[j * w + j];
+      if (!(p > kMinPivot) && lane == 0) s_bad = 1;
+      lp_mul(mu, eu, p);
+      const double rp = 1.0 / p;
+      const int r = w - j - 1;
+      for (int x = lane; x < r * r; x += 32) {
+        int i = j + 1 + x / r, l = j + 1 + x % r;
+        Wm[i * w + l] = fma(-Wm[i * w + j] * rp, Wm[j * w + l], Wm[i * w + l]);
+      }
+      __syncwarp();
+    }
+    // suffix Schur complement C = Wm[b.., b..] (CB x CB); each lane takes
+    // the lower triangle into registers and eliminates its F0..F4 pattern
+    double c[CB * (CB + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < CB; ++i)
+#pragma unroll
+      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = Wm[(b + i) * w + (b + l)];
+    __syncwarp();
+    double ml = mu;
+    int el = eu;
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < LANE_BITS; ++j) {
+      const bool inc = (lane >> j) & 1;
+      const double p = c[j * (j + 1) / 2 + j];
+      if (inc && !(p > kMinPivot)) bad = 1;
+      const double f = inc ? 1.0 / p : 0.0;
+      if (inc) lp_mul(ml, el, p);
+#pragma unroll
+      for (int i = j + 1; i < CB; ++i) {
+        const double ci = c[i * (i + 1) / 2 + j] * f;
+#pragma unroll
+        for (int l = j + 1; l <= i; ++l)
+          c[i * (i + 1) / 2 + l] = fma(-ci, c[l * (l + 1) / 2 + j], c[i * (i + 1) / 2 + l]);
+      }
+    }
+    constexpr int R = CB - LANE_BITS;
+    double a[R * (R + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int l = 0; l <= i; ++l)
+        a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
+    const int64_t blk = ((int64_t)blockIdx.x << b) | u;
+    Leaf<R>::run(a, ml, el, 0, table + blk * BLK, lane, &bad);
+    if (bad) s_bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0 && s_bad) atomicExch(flag, 1);
+}
+
+// Phase 2: one CTA per table block P.  Sums the leave-one-out neighbours
+// (the |P| neighbour blocks streamed from L2/HBM plus the in-block
+// neighbours from shared memory), forms the four measures and writes each
+// order's run at its lexicographic output position.
+__global__ void __launch_bounds__(256)
+k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
+                   const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
+                   int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane) {
+  __shared__ double own[BLK];
+  __shared__ double nbs[BLK];
+  __shared__ int64_t s_base[CB + 1];
+  constexpr int PER = BLK / 256;
+  const int tid = threadIdx.x;
+  const int64_t P = blockIdx.x;
+  const int kP = __popcll(P);
+  const int nP = N - CB;
+  // lexicographic base rank of each run (P u {first q suffix variables})
+  if (tid <= CB) {
+    const int q = tid, k = kP + q;
+    int64_t base = -1;
+    if (k >= kmin && k <= kmax && k >= 1) {
+      uint64_t r = binom(N, k) - 1;
+      int i = 0;
+      for (int j = 0; j < nP; ++j)
+        if ((P >> j) & 1) r -= binom(N - 1 - j, k - i++);
+      for (int t = 0; t < q; ++t) r -= binom(N - 1 - (nP + t), k - i++);
+      base = order_off[k - kmin] + (int64_t)r - g_begin;
+    }
+    s_base[q] = base;
+  }
+  __syncthreads();
+  // skip blocks with no output in [g_begin, g_end)
+  bool any = false;
+  for (int q = 0; q <= CB; ++q) {
+    int64_t b0 = s_base[q];
+    if (kP + q < kmin || kP + q > kmax || kP + q < 1) continue;
+    int64_t len = (int64_t)binom(CB, q);
+    if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
+  }
+  if (!any) return;
+  const double *tb = table + P * BLK;
+  double acc[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const double v = tb[tid + 256 * r];
+    own[tid + 256 * r] = v;
+    acc[r] = 0.0;
+  }
+  for (int j = 0; j < nP; ++j) {
+    if (!((P >> j) & 1)) continue;
+    const double *nb = table + (P ^ (1ll << j)) * BLK;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) acc[r] += nb[tid + 256 * r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int e = tid + 256 * r;
+    double s = acc[r];
+#pragma unroll
+    for (int t = 0; t < CB; ++t)
+      if ((e >> t) & 1) s += own[e ^ (1 << t)];
+    nbs[e] = s;
+  }
+  __syncthreads();
+  const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
+  const double e1 = et ? et[1] : 0.0;
+  for (int q = 0; q <= CB; ++q) {
+    const int k = kP + q;
+    if (k < kmin || k > kmax || k < 1) continue;
+    const int64_t b0 = s_base[q];
+    const int len = (int)binom(CB, q);
+    const int start = c_runstart[q];
+    const double kd = (double)k;
+    double ek = 0.0, ek1 = 0.0;
+    if (et) {
+      ek = et[k];
+      ek1 = et[k - 1];
+    }
+    for (int t = tid; t < len; t += 256) {
+      const int64_t row = b0 + t;
+      if (row < 0 || row >= g_end - g_begin) continue;
+      const int e = c_runmask[start + t];
+      const double l = own[e], nb = nbs[e];
+      double tc, dtc, o;
+      if (et) {
+        tc = -0.5 * l - kd * e1 + ek;
+        dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
+        o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+      } else {
+        tc = -0.5 * l;
+        dtc = 0.5 * ((1.0 - kd) * l + nb);
+        o = 0.5 * ((kd - 2.0) * l - nb);
+      }
+      const int64_t oi = row * D + d;
+      out[oi] = tc;
+      out[plane + oi] = dtc;
+      out[2 * plane + oi] = o;
+      out[3 * plane + oi] = tc + dtc;
+    }
+  }
+}
+
+void upload_tables() {
+  static thread_local int uploaded_for = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (uploaded_for == dev) return;
+  std::vector<uint16_t> lr(BLK), rm(BLK), rs(CB + 2);
+  std::vector<std::vector<int>> runs(CB + 1);
+  // lexicographic order of the q-subsets of {0..CB-1}: enumerate masks in
+  // tuple order by sorting
+  for (int q = 0; q <= CB; ++q) {
+    std::vector<std::vector<int>> tuples;
+    for (int mask = 0; mask < BLK; ++mask) {
+      if (__builtin_popcount(mask) != q) continue;
+      std::vector<int> t;
+      for (int b = 0; b < CB; ++b)
+        if ((mask >> b) & 1) t.push_back(b);
+      tuples.push_back(t);
+    }
+    std::sort(tuples.begin(), tuples.end());
+    for (size_t r = 0; r < tuples.size(); ++r) {
+      int mask = 0;
+      for (int b : tuples[r]) mask |= 1 << b;
+      lr[mask] = (uint16_t)r;
+      runs[q].push_back(mask);
+    }
+  }
+  int at = 0;
+  for (int q = 0; q <= CB; ++q) {
+    rs[q] = (uint16_t)at;
+    for (int mask : runs[q]) rm[at++] = (uint16_t)mask;
+  }
+  rs[CB + 1] = (uint16_t)at;
+  cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
+  cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
+  cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));
+  uploaded_for = dev;
+}
+
+}  // namespace
+
+bool lattice_available() { return true; }
+
+bool lattice_supports(int N) { return N >= CB + 2 && N <= MAXV; }
+
 int lattice_ws_bytes(int N, int D, size_t *bytes) {
-  (void)N; (void)D;
-  *bytes = 0;
-  return fail(HOI_INVALID_ARG, "lattice engine not built yet");
+  (void)D;
+  if (!lattice_supports(N)) return fail(HOI_INVALID_ARG, "lattice engine needs 12 <= N <= 32");
+  *bytes = (sizeof(double) << N) + 4096;
+  return HOI_OK;
 }
-int scan_full_lattice(const double *, const double *, int, int, int, int, int, int64_t, int64_t,
-                      double *, int32_t *, void *, size_t, cudaStream_t) {
-  return fail(HOI_INVALID_ARG, "lattice engine not built yet");
+
+// Workspace: [table 2^N doubles][flag int x16][order offsets int64 x33]
+struct LatticeWs {
+  double *table;
+  int *flag;
+  int64_t *offs;
+};
+
+static LatticeWs ws_view(void *ws, int N) {
+  LatticeWs w;
+  w.table = reinterpret_cast<double *>(ws);
+  w.flag = reinterpret_cast<int *>(reinterpret_cast<char *>(ws) + (sizeof(double) << N));
+  w.offs = reinterpret_cast<int64_t *>(w.flag + 16);
+  return w;
 }
+
+int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_bytes,
+                  cudaStream_t s) {
+  size_t need = 0;
+  int st = lattice_ws_bytes(N, D, &need);
+  if (st) return st;
+  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
+  LatticeWs w = ws_view(ws, N);
+  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+  const int nP = N - CB;
+  const int b = nP < MAXB ? nP : MAXB;
+  k_lattice_table<<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag);
+  return check_launch("k_lattice_table");
+}
+
+int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
+                     int kmax, int64_t g_begin, int64_t g_end, double *out, cudaStream_t s) {
+  upload_binomials();
+  upload_tables();
+  LatticeWs w = ws_view(ws, N);
+  int64_t h_off[MAXV + 1];
+  int64_t acc = 0;
+  for (int k = kmin; k <= kmax; ++k) {
+    h_off[k - kmin] = acc;
+    acc += (int64_t)host_binom(N, k);
+  }
+  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  k_lattice_measures<<<1u << (N - CB), 256, 0, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
+                                                    w.offs, g_begin, g_end, out, plane);
+  return check_launch("k_lattice_measures");
+}
+
+int lattice_status(void *ws, int N, cudaStream_t s) {
+  LatticeWs w = ws_view(ws, N);
+  int h_flag = 0;
+  cudaMemcpyAsync(&h_flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  if (h_flag) return fail(HOI_FALLBACK, "lattice: correlation matrix not numerically positive "
+                                        "definite; rerun with the per-n-plet engine");
+  return HOI_OK;
+}
+
+int scan_full_lattice(const double *corr, const double *eta, int kstride, int N, int D, int kmin,
+                      int kmax, int64_t g_begin, int64_t g_end, double *out, int32_t *err_count,
+                      void *ws, size_t ws_bytes, cudaStream_t s) {
+  (void)err_count;
+  for (int d = 0; d < D; ++d) {
+    int st = lattice_table(corr, N, D, d, ws, ws_bytes, s);
+    if (st) return st;
+    st = lattice_status(ws, N, s);
+    if (st) return st;
+    st = lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, s);
+    if (st) return st;
+  }
+  return HOI_OK;
+}
+
 }  // namespace hoib
-namespace hoib {
-bool lattice_available() { return false; }
+
+using namespace hoib;
+
+extern "C" int hoi_lattice_table(const double *corr, int32_t N, int32_t D, int32_t d, void *ws,
+                                 size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && d >= 0 && d < D, "hoi_lattice_table: bad args");
+  return lattice_table(corr, N, D, d, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, const double *eta,
+                                    int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
+                                    int64_t g_end, double *out, void *stream) {
+  HOI_CHECK_ARG(ws && out && lattice_supports(N) && d >= 0 && d < D && kmin >= 1 &&
+                    kmin <= kmax && kmax <= N && g_begin >= 0 && g_begin <= g_end,
+                "hoi_lattice_measures: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_measures: bias table too short");
+  return lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                          (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_status(void *ws, int32_t N, void *stream) {
+  HOI_CHECK_ARG(ws && lattice_supports(N), "hoi_lattice_status: bad args");
+  return lattice_status(ws, N, (cudaStream_t)stream);
 }

@@ -8,6 +8,7 @@ int scan_full_percell(const double *corr, const double *sdiag, const double *eta
                       cudaStream_t s);
 int lattice_ws_bytes(int N, int D, size_t *bytes);
 bool lattice_available();
+bool lattice_supports(int N);
 int scan_full_lattice(const double *corr, const double *eta, int kstride, int N, int D, int kmin,
                       int kmax, int64_t g_begin, int64_t g_end, double *out, int32_t *err_count,
                       void *ws, size_t ws_bytes, cudaStream_t s);
@@ -31,7 +32,7 @@ extern "C" int hoi_scan_full(const double *corr, const double *sdiag, const doub
   HOI_CHECK_ARG(g_begin >= 0 && g_begin <= g_end && (uint64_t)g_end <= total,
                 "hoi_scan_full: bad rank range");
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_scan_full: bias table too short");
-  if (engine == 0) engine = lattice_available() && N <= 34 && kmax >= 2 ? 2 : 1;
+  if (engine == 0) engine = lattice_available() && lattice_supports(N) ? 2 : 1;
   if (engine == 2) {
     size_t need = 0;
     int st = lattice_ws_bytes(N, D, &need);

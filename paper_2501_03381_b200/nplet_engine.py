@@ -187,7 +187,7 @@ def _raise_not_pd(err_count, err_coords, unravel=None):
     n = int(err_count.item())
     if n == 0:
         return
-    c = err_coords[: min(n, ERR_CAP)].cpu().numpy().reshape(-1, 2)
+    c = err_coords[: 2 * min(n, ERR_CAP)].cpu().numpy().reshape(-1, 2)
     coords = sorted((int(b), int(d)) for b, d in c)
     if unravel is not None:
         coords = sorted(unravel(b) for b, _ in coords)

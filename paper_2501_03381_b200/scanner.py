@@ -299,6 +299,29 @@ class _ScanCtx:
         self.engine = engine
         self.ws = None
         self.ws_bytes = ctypes.c_size_t(0)
+        self._alloc_ws()
+
+    def _args(self, g0, g1):
+        kst = 0 if self.eta is None else self.eta.shape[1]
+        return (self.st.corr.data_ptr(), self.st.sdiag.data_ptr(), nat.ptr(self.eta), kst,
+                self.n, self.d, self.lo, self.hi, g0, g1, self.engine)
+
+    def _alloc_ws(self):
+        """Query and allocate the engine workspace (the lattice engine's
+        2^N log-det table); auto mode drops to the per-n-plet engine when
+        the table does not fit."""
+        lib, torch = nat.lib(), self.torch
+        need = ctypes.c_size_t(0)
+        nat.check(lib.hoi_scan_full(*self._args(0, 0), None, None, None, 0, None,
+                                    ctypes.byref(need), None), "scan_full")
+        try:
+            self.ws = torch.empty(max(int(need.value), 8), dtype=torch.uint8, device="cuda")
+        except torch.cuda.OutOfMemoryError:
+            if self.engine != 0:
+                raise
+            self.engine = 1
+            self.ws = torch.empty(8, dtype=torch.uint8, device="cuda")
+        self.ws_bytes = ctypes.c_size_t(self.ws.numel())
 
     def full(self, g0, g1, out=None):
         torch, lib = self.torch, nat.lib()
@@ -306,18 +329,17 @@ class _ScanCtx:
         if out is None:
             out = torch.empty((4, rows, self.d), dtype=torch.float64, device="cuda")
         cnt, coords = _err_buffers(torch)
-        kst = 0 if self.eta is None else self.eta.shape[1]
-        args = (self.st.corr.data_ptr(), self.st.sdiag.data_ptr(), nat.ptr(self.eta), kst,
-                self.n, self.d, self.lo, self.hi, g0, g1, self.engine)
-        if self.ws is None:
-            need = ctypes.c_size_t(0)
-            nat.check(lib.hoi_scan_full(*args, None, None, None, 0, None, ctypes.byref(need), None),
-                      "scan_full")
-            self.ws = torch.empty(max(int(need.value), 8), dtype=torch.uint8, device="cuda")
-            self.ws_bytes = ctypes.c_size_t(self.ws.numel())
-        nat.check(lib.hoi_scan_full(*args, out.data_ptr(), cnt.data_ptr(), coords.data_ptr(),
-                                    ERR_CAP, self.ws.data_ptr(), ctypes.byref(self.ws_bytes),
-                                    nat.stream_handle(torch)), "scan_full")
+        rc = lib.hoi_scan_full(*self._args(g0, g1), out.data_ptr(), cnt.data_ptr(),
+                               coords.data_ptr(), ERR_CAP, self.ws.data_ptr(),
+                               ctypes.byref(self.ws_bytes), nat.stream_handle(torch))
+        if rc == nat.FALLBACK:
+            # the lattice engine declined (correlation not numerically PD):
+            # the per-n-plet engine applies the reference's jitter rule
+            self.engine = 1
+            self.ws = None
+            self._alloc_ws()
+            return self.full(g0, g1, out)
+        nat.check(rc, "scan_full")
         return out, cnt, coords
 
 
@@ -350,7 +372,7 @@ def _batch_bounds(n, lo, hi, batch_size):
 
 def _chunk_rows(d: int, torch) -> int:
     free, _ = torch.cuda.mem_get_info()
-    budget = min(int(free * 0.4), 8 << 30)
+    budget = min(int(free * 0.6), 64 << 30)
     return max(1 << 16, budget // (4 * 8 * d + 8 * 64))
 
 

@@ -9,6 +9,7 @@ REPO = Path(__file__).resolve().parents[1]
 GOLDEN = REPO / "tests" / "golden"
 sys.path.insert(0, str(REPO))
 sys.path.insert(0, str(REPO / "oracle"))
+sys.path.insert(0, str(REPO / "tests"))
 
 
 def pytest_configure(config):

@@ -48,7 +48,7 @@ def test_rank_copula_bit_exact(golden):
     np.testing.assert_array_equal(hoi.copula_transform(hoi.DataMatrix(g["x"])).values, g["z"])
     np.testing.assert_array_equal(hoi.rank_columns(g["tie"])[:, 0], [3, 1, 4, 2])
     cov = hoi.estimate_covariance(hoi.copula_transform(g["x"]))
-    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12)
+    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12, atol=1e-15)
     np.testing.assert_array_equal(cov.sigma, cov.sigma.T)
     assert cov.n_samples_used == 40
 
@@ -60,7 +60,7 @@ def test_copula_multichunk_with_ties(golden):
     r = hoi.rank_columns(x)
     assert hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest() == str(g["ranks_sha"])
     cov = hoi.estimate_covariance(hoi.copula_transform(x))
-    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12)
+    np.testing.assert_allclose(cov.sigma, g["cov"], rtol=1e-12, atol=1e-15)
     np.testing.assert_array_equal(cov.sigma, cov.sigma.T)
 
 
@@ -69,7 +69,7 @@ def test_copula_monotone_invariance_and_cfg4(golden):
     z = hoi.copula_transform(x).values
     np.testing.assert_array_equal(hoi.copula_transform(np.exp(x / 10.0)).values, z)
     cov = hoi.estimate_covariance(hoi.copula_transform(x))
-    np.testing.assert_allclose(cov.sigma, golden.npz("cfg4")["cov"], rtol=1e-12)
+    np.testing.assert_allclose(cov.sigma, golden.npz("cfg4")["cov"], rtol=1e-12, atol=1e-15)
 
 
 # -------------------------------------------------------- enumeration ---
@@ -322,3 +322,64 @@ def test_cfg5_batched_large_system(oracle):
     # the device copula path agrees with the oracle on one dataset
     cov0 = hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(0)))
     np.testing.assert_allclose(cov0.sigma, sig[0], rtol=1e-12, atol=1e-15)
+
+
+# ------------------------------------------------------ lattice engine --
+
+def _random_cov(n, seed):
+    rng = np.random.default_rng(seed)
+    r = workloads.randcorr(n, rng)
+    d = np.sqrt(rng.uniform(0.5, 3.0, n))
+    return r * np.outer(d, d)
+
+
+@pytest.mark.parametrize("n,lo,hi", [(12, 1, 12), (13, 2, 13), (16, 3, 9)])
+@pytest.mark.parametrize("bias", [False, True])
+def test_lattice_engine_vs_oracle(oracle, n, lo, hi, bias):
+    sig = _random_cov(n, n)
+    sig = 0.5 * (sig + sig.T)
+    covs = hoi.CovSet([hoi.CovarianceMatrix(sig, n_samples_used=500)])
+    dev = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=2)
+    _, vals = oracle.scan(sig, [500], lo, hi, oracle.CollectR(), bias=bias)
+    np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
+    # a sub-range of ranks lands at the same rows
+    total = hoi.count_nplets(n, lo, hi)
+    g0, g1 = total // 3, 2 * total // 3 + 1
+    part = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=2, g_begin=g0, g_end=g1)
+    np.testing.assert_array_equal(part.out.cpu().numpy(), dev.out[:, g0:g1].cpu().numpy())
+
+
+def test_lattice_matches_percell_engine_cfg3(golden):
+    g = golden.npz("cfg3")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    for bias in (False, True):
+        a = hoi.scan_device(covs, 3, 20, bias_correct=bias, engine=2).out
+        b = hoi.scan_device(covs, 3, 20, bias_correct=bias, engine=1).out
+        err = (a - b).abs() - 1e-9 * b.abs()
+        assert float(err.max()) <= 1e-11
+        assert bool((a[3] == a[0] + a[1]).all())
+
+
+def test_lattice_multi_dataset(oracle):
+    sigs = np.stack([_random_cov(14, s) for s in (1, 2, 3)])
+    sigs = 0.5 * (sigs + sigs.transpose(0, 2, 1))
+    covs = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=300) for s in sigs])
+    dev = hoi.scan_device(covs, 2, 14, bias_correct=True, engine=2)
+    _, vals = oracle.scan(sigs, [300] * 3, 2, 14, oracle.CollectR(), bias=True)
+    np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
+
+
+def test_lattice_declines_singular_covariance(oracle):
+    """A duplicated variable makes R singular: the lattice engine declines
+    and the per-n-plet engine applies the reference's jitter rule."""
+    sig = _random_cov(12, 7)
+    sig[11, :] = sig[10, :]
+    sig[:, 11] = sig[:, 10]
+    covs = hoi.CovSet([hoi.CovarianceMatrix(sig)])
+    dev = hoi.scan_device(covs, 2, 4)
+    _, vals = oracle.scan(sig, [0], 2, 4, oracle.CollectR())
+    got = dev.out.cpu().numpy()
+    assert np.isfinite(got).all()
+    rows = [c for k in range(2, 5) for c in itertools.combinations(range(12), k)]
+    clean = np.array([not (10 in r and 11 in r) for r in rows])
+    np.testing.assert_allclose(got[:, clean], vals[:, clean], rtol=RTOL, atol=ATOL)

@@ -94,3 +94,16 @@ def test_no_cpu_fallback():
         hoi.compute_hoi_batch(covs, hoi.NpletBatch(4, indices=np.array([[0, 1, 2]])))
     with pytest.raises(_native.BackendUnavailable):
         hoi.scan(covs, 2, 3, hoi.TopK("o", "max", 1))
+
+
+def test_lattice_layout_model_matches_oracle(oracle):
+    """The lattice engine's table layout, stencil and lexicographic run
+    placement (modelled in numpy by tests/lattice_model.py, mirroring
+    csrc/lattice.cu) reproduce the reference order and values."""
+    import lattice_model as lm
+    from paper_2501_03381_b200 import workloads
+    rng = np.random.default_rng(5)
+    r = workloads.randcorr(12, rng)
+    got = lm.measures_full(r, 2, 12)
+    rows, vals = oracle.scan(r, [0], 2, 12, oracle.CollectR())
+    np.testing.assert_allclose(got, vals[:, :, 0], rtol=1e-9, atol=1e-11)
