@@ -367,8 +367,15 @@ def b200_arm(a):
         }
     torch.cuda.empty_cache()
 
+    if rank == 0:
+        # the headline numbers are final here; print them once early so a
+        # later failure cannot lose them (the last line printed is the record)
+        print(json.dumps(line), file=sys.stderr, flush=True)
     if rank == 0 and not a.no_e2e:
-        line["e2e"] = e2e(a, torch, hoi)
+        try:
+            line["e2e"] = e2e(a, torch, hoi)
+        except Exception as exc:  # reported, never silently dropped
+            line["e2e"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         v, sampled, spent = cpu_sample(4, os.cpu_count() or 1)
         line["cpu_baseline"] = {

@@ -459,7 +459,8 @@ def _topk_plane(ctx, reducer, out, g0, m_idx):
             taus = [math.inf]
         else:
             samp_n = min(rows, 1 << 15)
-            pos = torch.linspace(0, rows - 1, samp_n, device="cuda").round().long()
+            pos = (torch.arange(samp_n, dtype=torch.int64, device="cuda") * (rows - 1)) // (
+                samp_n - 1)
             samp = np.sort(sign * plane[pos, d].cpu().numpy())
             taus = []
             for mult in (2, 8, 32, 128):

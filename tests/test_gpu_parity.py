@@ -187,8 +187,11 @@ def test_not_pd_coords_and_jitter(golden):
         _batched_logdet_invdiag(np.stack([np.eye(2), bad])[:, None])
     assert [list(c) for c in err.value.coords] == golden.meta["edge"]["npd_coords"]
     ld, idg = _batched_logdet_invdiag((np.ones((3, 3)) + np.eye(3) * 1e-14)[None, None])
+    # ones + 1e-14 I factors with ~1e-14 pivots on both sides (no jitter
+    # needed); those pivots carry ~1% rounding, so only finiteness and the
+    # magnitude are comparable (the reference test asserts finiteness)
     assert np.isfinite(ld).all()
-    np.testing.assert_allclose(ld, e["singular_ld"], rtol=1e-6)
+    assert abs(ld[0, 0] - e["singular_ld"][0, 0]) < 0.1
     # healthy matrices are unaffected by a failing neighbour (bit-identical)
     rng = np.random.default_rng(3)
     a = rng.standard_normal((8, 3))
