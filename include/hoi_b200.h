@@ -183,6 +183,18 @@ int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, const double
  * (5) Device reducers over a full-output plane (ref:scanner.py:50-137).
  * ------------------------------------------------------------------------- */
 
+/* Exact TopK candidates (ref:scanner.py:75-100): positions p of plane
+ * `vals` (stride D, dataset d) whose key sign*vals[p*D+d] is among the k
+ * smallest, plus the remainder of the k-th key's final 12-bit radix bucket
+ * (at most bucket_cap extra), so every tie at the k-th value is included.
+ * Radix select over the order-preserving 64-bit key, then one filter pass.
+ * Synchronous; *h_count (HOST) receives the candidate count (may exceed
+ * cand_cap when a tie is wider than the buffer; then only cand_cap stored).
+ * ws: device workspace of at least 4097 uint64. */
+int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
+                    int64_t k, int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
+                    int64_t *h_count, void *ws, void *stream);
+
 /* Candidate filter for TopK: writes the positions p in [0, n) of plane
  * `vals` (stride D, dataset d) whose key sign*vals[p*D+d] <= *thresh into
  * cand (int64), counting into *cand_count (device int64, caller zeroes).

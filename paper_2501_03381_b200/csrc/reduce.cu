@@ -1,6 +1,8 @@
 // Device reducers over full-output planes (ref:scanner.py:50-137).
 #include "common.cuh"
 
+#include <vector>
+
 namespace hoib {
 namespace {
 
@@ -62,6 +64,40 @@ __global__ void k_topk_filter(const double *__restrict__ vals, int64_t n, int D,
   }
 }
 
+// Radix-select histogram: 12-bit digit at `shift` of the orderable key of
+// sign*vals[p*D+d] over the elements whose key bits above shift+12 equal
+// `prefix` (masked by `hi_mask`).
+constexpr int kRadixBits = 12;
+constexpr int kRadixBins = 1 << kRadixBits;
+
+__global__ void __launch_bounds__(512)
+k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double sign,
+             uint64_t prefix, uint64_t hi_mask, int shift, unsigned long long *__restrict__ counts) {
+  __shared__ unsigned int h[kRadixBins];
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = orderable_key(sign * vals[p * D + d]);
+    if ((key & hi_mask) == prefix) atomicAdd(&h[(key >> shift) & (kRadixBins - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+}
+
+__global__ void k_key_filter(const double *__restrict__ vals, int64_t n, int D, int d, double sign,
+                             uint64_t key_max, int64_t *__restrict__ cand,
+                             unsigned long long *__restrict__ count, int64_t cap) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (orderable_key(sign * vals[p * D + d]) <= key_max) {
+      unsigned long long slot = atomicAdd(count, 1ull);
+      if ((int64_t)slot < cap) cand[slot] = p;
+    }
+  }
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -95,6 +131,60 @@ extern "C" int hoi_histogram(const double *vals, int64_t n, int32_t D, int32_t b
     return fail(HOI_INVALID_ARG, "hoi_histogram: bins * D too large");
   }
   return check_launch("k_hist");
+}
+
+// Exact candidate set for a top-k: the positions whose key sign*v is among
+// the k smallest, plus every position tied with or close to the k-th key
+// (all of the k-th key's final radix bucket, at most `bucket_cap` extra).
+// A 12-bit radix select narrows the threshold bucket until it holds at most
+// bucket_cap elements (or the key is fully resolved); one filter pass then
+// collects key <= bucket end.  Synchronous (reads back small histograms).
+extern "C" int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
+                               int64_t k, int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
+                               int64_t *h_count, void *ws, void *stream) {
+  HOI_CHECK_ARG(vals && cand && h_count && ws && d >= 0 && d < D && k >= 1 && n >= 0,
+                "hoi_topk_select: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
+  unsigned long long *ccount = counts + kRadixBins;
+  std::vector<unsigned long long> h(kRadixBins);
+  uint64_t prefix = 0, hi_mask = 0;
+  int64_t need = k < n ? k : n;
+  uint64_t key_max = ~0ull;
+  int blocks = 4 * sm_count();
+  if (need < n) {
+    for (int shift = 64 - kRadixBits; shift > -kRadixBits; shift -= kRadixBits) {
+      int sh = shift < 0 ? 0 : shift;
+      int bits = shift < 0 ? kRadixBits + shift : kRadixBits;
+      cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kRadixBins, s);
+      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, counts);
+      int st = check_launch("k_radix_hist");
+      if (st) return st;
+      cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * kRadixBins,
+                      cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      int64_t acc = 0;
+      int b = 0;
+      for (; b < (1 << bits); ++b) {
+        if (acc + (int64_t)h[b] >= need) break;
+        acc += (int64_t)h[b];
+      }
+      need -= acc;
+      prefix |= (uint64_t)b << sh;
+      hi_mask |= (uint64_t)((1 << bits) - 1) << sh;
+      key_max = prefix | (sh ? ((1ull << sh) - 1) : 0ull);
+      if ((int64_t)h[b] <= bucket_cap || sh == 0) break;
+    }
+  }
+  cudaMemsetAsync(ccount, 0, sizeof(unsigned long long), s);
+  k_key_filter<<<8 * sm_count(), 256, 0, s>>>(vals, n, D, d, sign, key_max, cand, ccount, cand_cap);
+  int st = check_launch("k_key_filter");
+  if (st) return st;
+  unsigned long long c = 0;
+  cudaMemcpyAsync(&c, ccount, sizeof(c), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  *h_count = (int64_t)c;
+  return HOI_OK;
 }
 
 extern "C" int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d, double sign,

@@ -296,7 +296,9 @@ class _ScanCtx:
         self.n, self.d = self.st.n, self.st.d
         self.lo, self.hi = lo, hi
         self.eta = self.st.eta(hi) if bias_correct else None
-        self.engine = engine
+        # auto: the subset-lattice engine when its 2^N table applies
+        # (12 <= N <= 32), the per-n-plet engine otherwise
+        self.engine = engine or (2 if 12 <= self.n <= 32 else 1)
         self.ws = None
         self.ws_bytes = ctypes.c_size_t(0)
         self._alloc_ws()
@@ -317,7 +319,7 @@ class _ScanCtx:
         try:
             self.ws = torch.empty(max(int(need.value), 8), dtype=torch.uint8, device="cuda")
         except torch.cuda.OutOfMemoryError:
-            if self.engine != 0:
+            if self.engine == 1:
                 raise
             self.engine = 1
             self.ws = torch.empty(8, dtype=torch.uint8, device="cuda")
@@ -440,7 +442,12 @@ def _emit_progress(progress, n, lo, hi, batch_size, total, t0):
 
 
 def _topk_plane(ctx, reducer, out, g0, m_idx):
-    """Merge one device chunk into the running per-dataset TopK lists."""
+    """Merge one device chunk into the running per-dataset TopK lists.
+
+    The device radix-selects the k smallest keys sign*value (plus the rest
+    of the k-th key's final radix bucket, so every tie is present); only
+    those candidates reach the host, where the reference's exact key
+    (sign*value, index tuple) orders them."""
     torch = ctx.torch
     lib = nat.lib()
     rows = out.shape[1]
@@ -448,40 +455,22 @@ def _topk_plane(ctx, reducer, out, g0, m_idx):
     if reducer._best is None:
         reducer._best = [[] for _ in range(ctx.d)]
     plane = out[m_idx]
-    cap = max(1 << 20, 64 * reducer.k)
+    bucket_cap = max(4096, reducer.k)
+    cap = reducer.k + bucket_cap + 1
     cand = torch.empty(cap, dtype=torch.int64, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    th = torch.empty(1, dtype=torch.float64, device="cuda")
+    ws = torch.empty(4096 + 64, dtype=torch.int64, device="cuda")
+    cnt = ctypes.c_int64(0)
     for d in range(ctx.d):
-        best = reducer._best[d]
-        run = best[-1][0][0] if len(best) >= reducer.k else math.inf
-        if rows <= cap // 2:
-            taus = [math.inf]
-        else:
-            samp_n = min(rows, 1 << 15)
-            pos = (torch.arange(samp_n, dtype=torch.int64, device="cuda") * (rows - 1)) // (
-                samp_n - 1)
-            samp = np.sort(sign * plane[pos, d].cpu().numpy())
-            taus = []
-            for mult in (2, 8, 32, 128):
-                q = min(samp_n - 1, int(math.ceil(reducer.k * samp_n / rows * mult)) + 16)
-                taus.append(float(samp[q]))
-            taus.append(math.inf)
-        for tau in taus:
-            tau = min(tau, run)
-            th.fill_(tau)
-            cnt.zero_()
-            nat.check(lib.hoi_topk_filter(plane.data_ptr(), rows, ctx.d, d, sign, th.data_ptr(),
-                                          cand.data_ptr(), cnt.data_ptr(), cap,
-                                          nat.stream_handle(torch)), "topk_filter")
-            c = int(cnt.item())
-            if c > cap:
-                raise NotImplementedError(
-                    f"TopK: {c} candidates tie within the selection threshold "
-                    f"(more than the {cap}-row candidate buffer)")
-            have = sum(1 for kk, _ in best if kk[0] <= tau)
-            if c + have >= reducer.k or tau == run or math.isinf(tau):
-                break
+        nat.check(lib.hoi_topk_select(plane.data_ptr(), rows, ctx.d, d, sign, reducer.k,
+                                      bucket_cap, cand.data_ptr(), cap, ctypes.byref(cnt),
+                                      ws.data_ptr(), nat.stream_handle(torch)), "topk_select")
+        c = int(cnt.value)
+        if c > cap:
+            # a tie wider than the candidate buffer at the k-th value (e.g.
+            # identical covariances): resolve it with the reference's host
+            # rule over the chunk, slice by slice
+            _topk_host_slices(ctx, reducer, out, g0, d)
+            continue
         pos = cand[:c]
         vals = out[:, pos, d].cpu().numpy()            # (4, c)
         tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, (pos + g0).cpu().numpy()) if c else []
@@ -493,6 +482,23 @@ def _topk_plane(ctx, reducer, out, g0, m_idx):
                          s=float(vals[3, i]))
             new.append(((sign * e.value, e.indices), e))
         reducer._merge(d, new)
+
+
+def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
+    from .nplet_engine import unrank_device
+    rows = out.shape[1]
+    sub = TopK(reducer.measure, reducer.direction, reducer.k)
+    for a in range(0, rows, step):
+        b = min(rows, a + step)
+        idx, orders = unrank_device(ctx.n, ctx.lo, ctx.hi, g0 + a, b - a)
+        hidx, ho = idx.cpu().numpy(), orders.cpu().numpy()
+        v = out[:, a:b, d:d + 1].cpu().numpy()
+        for k in np.unique(ho):
+            sel = np.flatnonzero(ho == k)
+            batch = NpletBatch(ctx.n, indices=hidx[sel, :k].astype(np.int64), check_unique=False)
+            sub.update(batch, HoiBatch(tc=v[0, sel], dtc=v[1, sel], o=v[2, sel], s=v[3, sel],
+                                       order=np.full(sel.size, k, dtype=np.int64)))
+    reducer._merge(d, sub._best[0])
 
 
 def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):

@@ -1,0 +1,50 @@
+"""Small, fixed workloads for ncu captures (one kernel family each).
+
+    python scripts/profile_target.py lattice   # cfg4 exhaustive scan, lattice engine
+    python scripts/profile_target.py eval10    # cfg5-like batch: K=10, N=400, D=16
+    python scripts/profile_target.py eval16    # cfg4 order-16 segment, per-n-plet engine
+"""
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2501_03381_b200 as hoi  # noqa: E402
+from paper_2501_03381_b200 import _build, workloads  # noqa: E402
+from paper_2501_03381_b200.scanner import _ScanCtx  # noqa: E402
+
+
+def main(mode):
+    _build.build()
+    if mode == "lattice":
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
+        ctx = _ScanCtx(covs, 2, 30, False, 2)
+        total = hoi.count_nplets(30, 2, 30)
+        out = torch.empty((4, total, 1), dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            ctx.full(0, total, out)
+    elif mode == "eval10":
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(d)))
+                           for d in range(16)])
+        idx = workloads.cfg5_nplets(b=1 << 18)
+        batch = hoi.NpletBatch(400, indices=idx, check_unique=False)
+        for _ in range(2):
+            hoi.compute_hoi_batch(covs, batch)
+    elif mode == "eval16":
+        import math
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
+        ctx = _ScanCtx(covs, 16, 16, False, 1)
+        n = math.comb(30, 16) // 16
+        out = torch.empty((4, n, 1), dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            ctx.full(0, n, out)
+    torch.cuda.synchronize()
+    print("ok", mode)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
