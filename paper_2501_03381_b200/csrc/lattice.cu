@@ -26,6 +26,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 namespace hoib {
@@ -43,6 +44,7 @@ constexpr double LN2 = 0.69314718055994530942;
 // reference's per-matrix jitter rule) takes the scan.
 constexpr double kMinPivot = 1e-12;
 
+__constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
 __constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
 __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
@@ -57,19 +59,40 @@ __device__ __forceinline__ void lp_mul(double &m, int &e, double x) {
   }
 }
 
-__device__ __forceinline__ double lp_log(double m, int e) {
-  double l = log(m);
-  return e == 0 ? l : l + (double)e * LN2;
+// Table-driven FP64 natural log of m * 2^e_extra (m > 0 normal): with
+// x = 2^e * f, f in [1,2), j = top 8 bits of f, c_j = RN(1/(1+j/256)) and
+// L_j = -log(c_j) (host-evaluated in 80-bit precision), r = f*c_j - 1 lies in
+// [0, 2^-8) and log x = e*ln2 + L_j + log1p(r) with a degree-8 polynomial
+// (truncation < 2^-67).  ~12 FP64 instructions against ~40 for log(); exact
+// 0 for x = 1 (c_0 = 1, L_0 = 0), so identity blocks keep exact zeros.
+__device__ __forceinline__ double fast_log(double m, int e_extra, const double2 *__restrict__ tab) {
+  const long long b = __double_as_longlong(m);
+  const int e = (int)((b >> 52) & 0x7FF) - 1023 + e_extra;
+  const int j = (int)((b >> 44) & 0xFF);
+  const double f = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+  const double2 t = tab[j];
+  const double r = fma(f, t.x, -1.0);
+  double p = fma(r, -0.125, 0.14285714285714285);
+  p = fma(r, p, -0.16666666666666666);
+  p = fma(r, p, 0.2);
+  p = fma(r, p, -0.25);
+  p = fma(r, p, 0.33333333333333331);
+  p = fma(r, p, -0.5);
+  p = fma(r, p, 1.0);
+  const double ed = (double)e;
+  return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(r, p, t.y)));
 }
 
 // Leaf recursion over the last R suffix variables held in registers as a
 // packed lower triangle.  Include/exclude variable 0 of the remainder; the
 // include branch takes the Schur complement.  2^R leaves, one log each.
+// The running pivot product m enters normalised to [0.5, 1) and picks up at
+// most R factors in [1e-12, 1], so it cannot underflow inside the recursion.
 template <int R>
 struct Leaf {
   static __device__ __forceinline__ void run(const double (&a)[R * (R + 1) / 2], double m, int e,
                                              int bits, double *__restrict__ out, int lane,
-                                             int *bad) {
+                                             int &bad, const double2 *__restrict__ tab) {
     constexpr int R1 = R - 1;
     double ex[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
     // exclude variable (CB - R): remainder unchanged
@@ -77,10 +100,10 @@ struct Leaf {
     for (int i = 1; i < R; ++i)
 #pragma unroll
       for (int l = 1; l <= i; ++l) ex[(i - 1) * i / 2 + (l - 1)] = a[i * (i + 1) / 2 + l];
-    Leaf<R1>::run(ex, m, e, bits, out, lane, bad);
+    Leaf<R1>::run(ex, m, e, bits, out, lane, bad, tab);
     // include: pivot a00, Schur complement of the rest
     const double p = a[0];
-    if (!(p > kMinPivot)) *bad = 1;
+    bad |= !(p > kMinPivot);
     const double rp = 1.0 / p;
     double in[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
 #pragma unroll
@@ -90,28 +113,27 @@ struct Leaf {
       for (int l = 1; l <= i; ++l)
         in[(i - 1) * i / 2 + (l - 1)] = fma(-ai, a[l * (l + 1) / 2], a[i * (i + 1) / 2 + l]);
     }
-    double m2 = m;
-    int e2 = e;
-    lp_mul(m2, e2, p);
-    Leaf<R1>::run(in, m2, e2, bits | (1 << (CB - R)), out, lane, bad);
+    Leaf<R1>::run(in, m * p, e, bits | (1 << (CB - R)), out, lane, bad, tab);
   }
 };
 
 template <>
 struct Leaf<0> {
   static __device__ __forceinline__ void run(const double (&)[1], double m, int e, int bits,
-                                             double *__restrict__ out, int lane, int *) {
+                                             double *__restrict__ out, int lane, int &,
+                                             const double2 *__restrict__ tab) {
     // bits holds the F5..F9 pattern at bit positions 5..9
-    out[bits + lane] = lp_log(m, e);
+    out[bits + lane] = fast_log(m, e, tab);
   }
 };
 
 // Phase 1: one CTA per pattern of the "fixed" prefix variables b..N-CB-1;
 // its 8 warps expand the 2^b patterns of prefix variables 0..b-1, and each
 // lane of a warp owns one pattern of F0..F4 and recurses over F5..F9.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
                 double *__restrict__ table, int *__restrict__ flag) {
+  __shared__ double2 s_logtab[256];
   constexpr int MS = MAXV + 1;
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
   __shared__ double W[8][(MAXB + CB) * (MAXB + CB)];  // per-warp (b+CB)^2 work
@@ -122,6 +144,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nP = N - CB;
+  s_logtab[tid] = c_logtab[tid];
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
@@ -215,7 +238,12 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       for (int l = 0; l <= i; ++l)
         a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
     const int64_t blk = ((int64_t)blockIdx.x << b) | u;
-    Leaf<R>::run(a, ml, el, 0, table + blk * BLK, lane, &bad);
+    {
+      int ex;
+      ml = frexp(ml, &ex);
+      el += ex;
+    }
+    Leaf<R>::run(a, ml, el, 0, table + blk * BLK, lane, bad, s_logtab);
     if (bad) s_bad = 1;
   }
   __syncthreads();
@@ -316,11 +344,13 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
         dtc = 0.5 * ((1.0 - kd) * l + nb);
         o = 0.5 * ((kd - 2.0) * l - nb);
       }
+      // streaming (evict-first) stores: the 32 B/n-plet output must not
+      // push the log-det table's neighbour blocks out of L2
       const int64_t oi = row * D + d;
-      out[oi] = tc;
-      out[plane + oi] = dtc;
-      out[2 * plane + oi] = o;
-      out[3 * plane + oi] = tc + dtc;
+      __stcs(out + oi, tc);
+      __stcs(out + plane + oi, dtc);
+      __stcs(out + 2 * plane + oi, o);
+      __stcs(out + 3 * plane + oi, tc + dtc);
     }
   }
 }
@@ -357,6 +387,14 @@ void upload_tables() {
     for (int mask : runs[q]) rm[at++] = (uint16_t)mask;
   }
   rs[CB + 1] = (uint16_t)at;
+  std::vector<double2> lt(256);
+  for (int j = 0; j < 256; ++j) {
+    long double c = 1.0L / (1.0L + (long double)j / 256.0L);
+    double cd = (double)c;
+    lt[j].x = cd;
+    lt[j].y = (double)(-logl((long double)cd));
+  }
+  cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * 256);
   cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));
@@ -397,6 +435,7 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   int st = lattice_ws_bytes(N, D, &need);
   if (st) return st;
   if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
+  upload_tables();
   LatticeWs w = ws_view(ws, N);
   cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   const int nP = N - CB;
