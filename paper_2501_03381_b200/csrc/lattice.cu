@@ -43,6 +43,10 @@ constexpr double LN2 = 0.69314718055994530942;
 // noise, so the engine declines and the per-n-plet engine (with the
 // reference's per-matrix jitter rule) takes the scan.
 constexpr double kMinPivot = 1e-12;
+// Block-index bits whose neighbour blocks lie beyond the L2 reuse window
+// (126 MB / 8 KB blocks ~ 2^14 blocks): streamed with evict-first loads.
+constexpr int kFarBits = 6;
+constexpr int kMinNearBits = 12;
 
 __constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
@@ -290,29 +294,55 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
   }
   if (!any) return;
-  const double *tb = table + P * BLK;
-  double acc[PER];
-#pragma unroll
-  for (int r = 0; r < PER; ++r) {
-    const double v = tb[tid + 256 * r];
-    own[tid + 256 * r] = v;
-    acc[r] = 0.0;
+  // Thread tid owns entries {2tid, 2tid+1, 512+2tid, 513+2tid} (16-byte loads).
+  // Neighbour blocks along the low block bits were touched a few thousand
+  // CTAs earlier and are served from L2 (ld.cg); blocks along the top
+  // kFarBits bits were not, so they are streamed with evict-first loads
+  // (ld.cs) instead of displacing the reusable near window.
+  const double2 *tb = reinterpret_cast<const double2 *>(table + P * BLK);
+  const double2 o0 = __ldcg(tb + tid), o1 = __ldcg(tb + 256 + tid);
+  reinterpret_cast<double2 *>(own)[tid] = o0;
+  reinterpret_cast<double2 *>(own)[256 + tid] = o1;
+  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  const int near_bits = nP > kFarBits + kMinNearBits ? nP - kFarBits : nP;
+  const uint32_t near_mask = (1u << near_bits) - 1u;
+  uint32_t near = (uint32_t)P & near_mask, far = (uint32_t)P & ~near_mask;
+  while (near) {
+    const int j0 = __ffs(near) - 1;
+    near &= near - 1;
+    const double2 *n0 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j0)) * BLK);
+    const double2 x0 = __ldcg(n0 + tid), y0 = __ldcg(n0 + 256 + tid);
+    if (near) {
+      const int j1 = __ffs(near) - 1;
+      near &= near - 1;
+      const double2 *n1 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j1)) * BLK);
+      const double2 x1 = __ldcg(n1 + tid), y1 = __ldcg(n1 + 256 + tid);
+      a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
+      a0.x += x1.x; a0.y += x1.y; a1.x += y1.x; a1.y += y1.y;
+    } else {
+      a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
+    }
   }
-  for (int j = 0; j < nP; ++j) {
-    if (!((P >> j) & 1)) continue;
-    const double *nb = table + (P ^ (1ll << j)) * BLK;
-#pragma unroll
-    for (int r = 0; r < PER; ++r) acc[r] += nb[tid + 256 * r];
+  while (far) {
+    const int j0 = __ffs(far) - 1;
+    far &= far - 1;
+    const double2 *n0 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j0)) * BLK);
+    const double2 x0 = __ldcs(n0 + tid), y0 = __ldcs(n0 + 256 + tid);
+    a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
   }
   __syncthreads();
+  {
+    const int es[4] = {2 * tid, 2 * tid + 1, 512 + 2 * tid, 513 + 2 * tid};
+    const double as[4] = {a0.x, a0.y, a1.x, a1.y};
 #pragma unroll
-  for (int r = 0; r < PER; ++r) {
-    const int e = tid + 256 * r;
-    double s = acc[r];
+    for (int r = 0; r < PER; ++r) {
+      const int e = es[r];
+      double s = as[r];
 #pragma unroll
-    for (int t = 0; t < CB; ++t)
-      if ((e >> t) & 1) s += own[e ^ (1 << t)];
-    nbs[e] = s;
+      for (int t = 0; t < CB; ++t)
+        if ((e >> t) & 1) s += own[e ^ (1 << t)];
+      nbs[e] = s;
+    }
   }
   __syncthreads();
   const double *et = eta ? eta + (int64_t)d * kstride : nullptr;

@@ -44,6 +44,22 @@ def main():
               f"ctx {1e3*(t4-t3):.1f} scan {1e3*(t5-t4):.1f} topk {1e3*(t6-t5):.1f} "
               f"fin {1e3*(t7-t6):.1f} ms; {len(res[0])} entries")
         del out
+    import cProfile
+    import pstats
+    for it in range(3):
+        t0 = t()
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(hoi.DataMatrix(x)))])
+        t1 = t()
+        pr = cProfile.Profile() if it == 2 else None
+        if pr:
+            pr.enable()
+        res = hoi.scan(covs, 2, 30, hoi.TopK("o", "min", 1000))
+        t2 = t()
+        if pr:
+            pr.disable()
+            pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+        print(f"public api iter {it}: covs {1e3*(t1-t0):.1f} ms scan+topk {1e3*(t2-t1):.1f} ms "
+              f"({len(res[0])} entries)")
 
 
 if __name__ == "__main__":
