@@ -325,15 +325,35 @@ class _ScanCtx:
             self.ws = torch.empty(8, dtype=torch.uint8, device="cuda")
         self.ws_bytes = ctypes.c_size_t(self.ws.numel())
 
-    def full(self, g0, g1, out=None):
+    def full(self, g0, g1, out=None, reuse_table=False):
+        """Full output (4, g1-g0, D) for global ranks [g0, g1).
+
+        reuse_table: for the lattice engine with one dataset, keep the log-det
+        table of a previous call (a scan split into several rank chunks
+        builds it once)."""
         torch, lib = self.torch, nat.lib()
         rows = g1 - g0
         if out is None:
             out = torch.empty((4, rows, self.d), dtype=torch.float64, device="cuda")
         cnt, coords = _err_buffers(torch)
-        rc = lib.hoi_scan_full(*self._args(g0, g1), out.data_ptr(), cnt.data_ptr(),
-                               coords.data_ptr(), ERR_CAP, self.ws.data_ptr(),
-                               ctypes.byref(self.ws_bytes), nat.stream_handle(torch))
+        s = nat.stream_handle(torch)
+        if self.engine == 2 and self.d == 1:
+            rc = nat.OK
+            if not (reuse_table and getattr(self, "_table_ok", False)):
+                self._table_ok = False
+                rc = lib.hoi_lattice_table(self.st.corr.data_ptr(), self.n, 1, 0,
+                                           self.ws.data_ptr(), self.ws.numel(), s)
+                if rc == nat.OK:
+                    rc = lib.hoi_lattice_status(self.ws.data_ptr(), self.n, s)
+                self._table_ok = rc == nat.OK
+            if rc == nat.OK:
+                kst = 0 if self.eta is None else self.eta.shape[1]
+                rc = lib.hoi_lattice_measures(self.ws.data_ptr(), self.n, 1, 0, nat.ptr(self.eta),
+                                              kst, self.lo, self.hi, g0, g1, out.data_ptr(), s)
+        else:
+            rc = lib.hoi_scan_full(*self._args(g0, g1), out.data_ptr(), cnt.data_ptr(),
+                                   coords.data_ptr(), ERR_CAP, self.ws.data_ptr(),
+                                   ctypes.byref(self.ws_bytes), s)
         if rc == nat.FALLBACK:
             # the lattice engine declined (correlation not numerically PD):
             # the per-n-plet engine applies the reference's jitter rule
@@ -372,9 +392,11 @@ def _batch_bounds(n, lo, hi, batch_size):
         off += c
 
 
-def _chunk_rows(d: int, torch) -> int:
+def _chunk_rows(d: int, torch, cap_bytes: int = 64 << 30) -> int:
     free, _ = torch.cuda.mem_get_info()
-    budget = min(int(free * 0.6), 64 << 30)
+    # memory held in torch's cache is free for our next allocation too
+    free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+    budget = min(int(free * 0.6), cap_bytes)
     return max(1 << 16, budget // (4 * 8 * d + 8 * 64))
 
 
@@ -397,7 +419,7 @@ def _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0):
     torch = ctx.torch
     from .nplet_engine import unrank_device
     bounds = list(_batch_bounds(ctx.n, ctx.lo, ctx.hi, batch_size))
-    per_chunk = _chunk_rows(ctx.d, torch)
+    per_chunk = _chunk_rows(ctx.d, torch, cap_bytes=1 << 30)   # host-side staging size
     i, seen, nb = 0, 0, 0
     while i < len(bounds):
         j, rows = i, 0
@@ -405,7 +427,7 @@ def _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0):
             rows += bounds[j][1] - bounds[j][0]
             j += 1
         g0, g1 = bounds[i][0], bounds[j - 1][1]
-        out, cnt, coords = ctx.full(g0, g1)
+        out, cnt, coords = ctx.full(g0, g1, reuse_table=i > 0)
         try:
             _raise_not_pd(cnt, coords)
         except Exception as e:  # map to the reference's per-batch coordinates
@@ -512,7 +534,7 @@ def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):
     g0 = 0
     while g0 < total:
         g1 = min(total, g0 + per_chunk)
-        out, cnt, coords = ctx.full(g0, g1)
+        out, cnt, coords = ctx.full(g0, g1, reuse_table=g0 > 0)
         _raise_not_pd(cnt, coords)
         if hist_counts is not None:
             nat.check(nat.lib().hoi_histogram(
