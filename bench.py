@@ -96,11 +96,11 @@ def reference_arm(a):
     workers = os.cpu_count() or 1
     vals = []
     for i in range(a.warmup + a.steps):
-        v, sampled, spent = cpu_sample(1, workers)
+        v, sampled, spent = cpu_sample(workers, workers)
         if i >= a.warmup:
             vals.append(v)
     value = float(np.median(vals))
-    sample = (f"first batch (<=10,000 n-plets) of each order 2..30 per step, "
+    sample = (f"first {workers} batches (<=10,000 n-plets each, one per worker thread) of each order 2..30 per step, "
               f"{sampled} n-plets/step, extrapolated by C(30,k)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "n-plets/s",
@@ -377,10 +377,10 @@ def b200_arm(a):
         except Exception as exc:  # reported, never silently dropped
             line["e2e"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, sampled, spent = cpu_sample(4, os.cpu_count() or 1)
+        v, sampled, spent = cpu_sample(os.cpu_count() or 1, os.cpu_count() or 1)
         line["cpu_baseline"] = {
             "value": v, "unit": "n-plets/s", "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"first 4 batches of 10,000 n-plets of every order 2..30 "
+            "sample": f"first <cores> batches of 10,000 n-plets of every order 2..30 "
                       f"({sampled} n-plets, {spent:.1f} s) through the oracle port of the "
                       f"reference algorithm, extrapolated by C(30,k)"}
     if rank == 0:

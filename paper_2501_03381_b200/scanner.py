@@ -392,12 +392,14 @@ def _batch_bounds(n, lo, hi, batch_size):
         off += c
 
 
-def _chunk_rows(d: int, torch, cap_bytes: int = 64 << 30) -> int:
+def _chunk_rows(d: int, torch, cap_bytes: int = 64 << 30, extra_per_row: int = 0) -> int:
+    """Rows per device chunk: 32 B x D of output per row (+ any per-row
+    staging) within 60% of the free device memory, capped at cap_bytes."""
     free, _ = torch.cuda.mem_get_info()
     # memory held in torch's cache is free for our next allocation too
     free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     budget = min(int(free * 0.6), cap_bytes)
-    return max(1 << 16, budget // (4 * 8 * d + 8 * 64))
+    return max(1 << 16, budget // (4 * 8 * d + extra_per_row))
 
 
 def _unrank_list(n, lo, hi, ranks):
@@ -419,7 +421,8 @@ def _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0):
     torch = ctx.torch
     from .nplet_engine import unrank_device
     bounds = list(_batch_bounds(ctx.n, ctx.lo, ctx.hi, batch_size))
-    per_chunk = _chunk_rows(ctx.d, torch, cap_bytes=1 << 30)   # host-side staging size
+    # host-side staging size; unranked indices add 4 B x max order per row
+    per_chunk = _chunk_rows(ctx.d, torch, cap_bytes=1 << 30, extra_per_row=4 * ctx.hi)
     i, seen, nb = 0, 0, 0
     while i < len(bounds):
         j, rows = i, 0
