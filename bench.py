@@ -240,6 +240,37 @@ def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
             "kernel_share_of_step": (tm + tt) / step_ms}
 
 
+def fused_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
+    """CUDA-event timing of the single fused lattice kernel (k_lattice_fused):
+    HBM-bound; algorithmic bytes = the 2^N log-det table written once and read
+    once + 32 B per n-plet written."""
+    s = nat.stream_handle(torch)
+    ws = ctx.ws
+    ts = []
+    for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        nat.check(lib.hoi_lattice_fused(ctx.st.corr.data_ptr(), N, 1, 0, None, 0, LO, HI, g0, g1,
+                                        out.data_ptr(), ws.data_ptr(), ws.numel(), s))
+        ev[1].record()
+        torch.cuda.synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]))
+    t = float(np.mean(ts))
+    alg = 2 * 8 * (1 << N) + 32 * (g1 - g0)
+    peak, src = measured_peaks()
+    achieved = alg / (t * 1e-3) / 1e9
+    traffic = None
+    tf = REPO / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("k_lattice_fused_bytes")
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "k_lattice_fused (log-det table + leave-one-out stencil + epilogue, one pass)",
+            "peak_source": src, "algorithmic_bytes_per_launch": alg,
+            "algorithmic_bytes_note": "8 B x 2^N table written + read once, 32 B x n-plets written",
+            "kernel_ms": t, "kernel_share_of_step": t / step_ms}
+
+
 def percell_roofline(torch, lib, nat, covs, g0, g1, step_ms):
     """FP64 roofline of the per-n-plet engine (k_eval<K>: LDL^T + inverse
     diagonal + epilogue) on the same workload: one CUDA-event-timed launch
@@ -340,6 +371,8 @@ def b200_arm(a):
     roof = None
     if rank == 0 and engine_used == 2:
         roof = lattice_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
+    if rank == 0 and engine_used == 3:
+        roof = fused_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     del out
     torch.cuda.empty_cache()
     fp64 = None

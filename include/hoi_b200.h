@@ -179,6 +179,14 @@ int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, const double
                          int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
                          int64_t g_end, double *out, void *stream);
 
+/* Engine 3: both phases in ONE persistent pass (dataset d).  Warps claim
+ * table blocks in increasing order, build and publish their block, then
+ * acquire their (lower-index, already claimed) neighbour blocks and write
+ * the measures.  Synchronous (returns HOI_FALLBACK if not PD). */
+int hoi_lattice_fused(const double *corr, int32_t N, int32_t D, int32_t d, const double *eta,
+                      int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
+                      int64_t g_end, double *out, void *ws, size_t ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------
  * (5) Device reducers over a full-output plane (ref:scanner.py:50-137).
  * ------------------------------------------------------------------------- */

@@ -48,6 +48,8 @@ _SIGS = {
     "hoi_lattice_status": ([_vp, _i32, _vp], C.c_int),
     "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,
                               _vp], C.c_int),
+    "hoi_lattice_fused": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp, _vp,
+                           _sz, _vp], C.c_int),
     "hoi_topk_select": ([_vp, _i64, _i32, _i32, _dbl, _i64, _i64, _vp, _i64, C.POINTER(_i64),
                          _vp, _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),

@@ -385,6 +385,228 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused engine-2 pass: one persistent warp per CTA claims table blocks in
+// increasing index order, PRODUCES T[P] (Schur elimination of P's prefix
+// variables + the register leaf recursion), publishes it (release flag),
+// then CONSUMES P: every neighbour block P ^ (1<<j) has a smaller index, so
+// it was claimed earlier by a running CTA whose production never waits --
+// the acquire-wait always terminates.  The own block never round-trips
+// through HBM and the FP64 table work overlaps the output stream.
+// ---------------------------------------------------------------------------
+__device__ double2 g_logtab[256];
+
+constexpr long long kSpinLimit = 20000000000ll;   // ~10 s at 2 GHz: fail loudly, never hang
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, int kmax,
+                const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
+                int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
+                double *__restrict__ table, unsigned *__restrict__ flags,
+                unsigned *__restrict__ counter, int *__restrict__ err) {
+  __shared__ __align__(16) double own[BLK];
+  __shared__ __align__(16) double nbs[BLK];       // also the gathered matrix while producing
+  __shared__ int vars[MAXV];
+  __shared__ int64_t s_base[CB + 1];
+  const int lane = threadIdx.x;
+  const int nP = N - CB;
+  const unsigned nblocks = 1u << nP;
+  const double2 *logtab = g_logtab;
+  const int near_bits = nP > kFarBits + kMinNearBits ? nP - kFarBits : nP;
+  for (;;) {
+    unsigned P = 0;
+    if (lane == 0) P = atomicAdd(counter, 1u);
+    P = __shfl_sync(0xffffffffu, P, 0);
+    if (P >= nblocks) break;
+    // ------------------------------------------------ produce T[P] ----
+    const int nfix = __popc(P);
+    const int m = nfix + CB;
+    if (lane == 0) {
+      int nf = 0;
+      for (int j = 0; j < nP; ++j)
+        if ((P >> j) & 1) vars[nf++] = j;
+      for (int t = 0; t < CB; ++t) vars[nf + t] = nP + t;
+    }
+    __syncwarp();
+    double *M = nbs;                                  // m <= 32 -> m*m <= 1024
+    for (int x = lane; x < m * m; x += 32) {
+      const int i = x / m, l = x - i * m;
+      M[x] = __ldg(corr + ((int64_t)vars[i] * N + vars[l]) * D + d);
+    }
+    __syncwarp();
+    double m0 = 1.0;
+    int e0 = 0;
+    int bad = 0;
+    for (int j = 0; j < nfix; ++j) {
+      const double p = M[j * m + j];
+      bad |= !(p > kMinPivot);
+      lp_mul(m0, e0, p);
+      const double rp = 1.0 / p;
+      const int r = m - j - 1;
+      for (int x = lane; x < r * r; x += 32) {
+        const int i = j + 1 + x / r, l = j + 1 + x % r;
+        M[i * m + l] = fma(-M[i * m + j] * rp, M[j * m + l], M[i * m + l]);
+      }
+      __syncwarp();
+    }
+    double c[CB * (CB + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < CB; ++i)
+#pragma unroll
+      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = M[(nfix + i) * m + (nfix + l)];
+    double ml = m0;
+    int el = e0;
+#pragma unroll
+    for (int j = 0; j < LANE_BITS; ++j) {
+      const bool inc = (lane >> j) & 1;
+      const double p = c[j * (j + 1) / 2 + j];
+      if (inc && !(p > kMinPivot)) bad = 1;
+      const double f = inc ? 1.0 / p : 0.0;
+      if (inc) lp_mul(ml, el, p);
+#pragma unroll
+      for (int i = j + 1; i < CB; ++i) {
+        const double ci = c[i * (i + 1) / 2 + j] * f;
+#pragma unroll
+        for (int l = j + 1; l <= i; ++l)
+          c[i * (i + 1) / 2 + l] = fma(-ci, c[l * (l + 1) / 2 + j], c[i * (i + 1) / 2 + l]);
+      }
+    }
+    {
+      int ex;
+      ml = frexp(ml, &ex);
+      el += ex;
+    }
+    constexpr int R = CB - LANE_BITS;
+    double a[R * (R + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int l = 0; l <= i; ++l)
+        a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
+    Leaf<R>::run(a, ml, el, 0, own, lane, bad, logtab);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
+    __syncwarp();
+    // publish: table block to HBM (kept in L2 for the near consumers)
+    {
+      const double2 *o2 = reinterpret_cast<const double2 *>(own);
+      double2 *t2 = reinterpret_cast<double2 *>(table + (int64_t)P * BLK);
+#pragma unroll 4
+      for (int x = lane; x < BLK / 2; x += 32) __stcg(t2 + x, o2[x]);
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(flags + P, 1u);
+    // ------------------------------------------------ consume P ------
+    // lane owns entries e = 64 x + 2 lane + {0,1}, x = 0..15
+    double2 acc[BLK / 64];
+#pragma unroll
+    for (int x = 0; x < BLK / 64; ++x) acc[x] = make_double2(0.0, 0.0);
+    uint32_t rem = P;
+    while (rem) {
+      const int j = 31 - __clz(rem);                 // far (high) bits first
+      rem &= ~(1u << j);
+      const unsigned Pn = P ^ (1u << j);
+      if (lane == 0) {
+        long long t0 = clock64();
+        while (ld_acquire(flags + Pn) == 0u) {
+          if (clock64() - t0 > kSpinLimit) {
+            atomicExch(err, 2);
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      const double2 *nb = reinterpret_cast<const double2 *>(table + (int64_t)Pn * BLK);
+      if (j >= near_bits) {
+#pragma unroll
+        for (int x = 0; x < BLK / 64; ++x) {
+          const double2 v = __ldcs(nb + 32 * x + lane);
+          acc[x].x += v.x;
+          acc[x].y += v.y;
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < BLK / 64; ++x) {
+          const double2 v = __ldcg(nb + 32 * x + lane);
+          acc[x].x += v.x;
+          acc[x].y += v.y;
+        }
+      }
+    }
+    // lexicographic base rank of each run
+    const int kP = nfix;
+    if (lane <= CB) {
+      const int q = lane, k = kP + q;
+      int64_t base = -1;
+      if (k >= kmin && k <= kmax && k >= 1) {
+        uint64_t r = binom(N, k) - 1;
+        int i = 0;
+        for (int j = 0; j < nP; ++j)
+          if ((P >> j) & 1) r -= binom(N - 1 - j, k - i++);
+        for (int t = 0; t < q; ++t) r -= binom(N - 1 - (nP + t), k - i++);
+        base = order_off[k - kmin] + (int64_t)r - g_begin;
+      }
+      s_base[q] = base;
+    }
+#pragma unroll
+    for (int x = 0; x < BLK / 64; ++x) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 64 * x + 2 * lane + h;
+        double s = h ? acc[x].y : acc[x].x;
+#pragma unroll
+        for (int t = 0; t < CB; ++t)
+          if ((e >> t) & 1) s += own[e ^ (1 << t)];
+        nbs[e] = s;
+      }
+    }
+    __syncwarp();
+    const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
+    const double e1 = et ? et[1] : 0.0;
+    for (int q = 0; q <= CB; ++q) {
+      const int k = kP + q;
+      if (k < kmin || k > kmax || k < 1) continue;
+      const int64_t b0 = s_base[q];
+      const int len = (int)binom(CB, q);
+      const int start = c_runstart[q];
+      const double kd = (double)k;
+      const double ek = et ? et[k] : 0.0, ek1 = et ? et[k - 1] : 0.0;
+      for (int t = lane; t < len; t += 32) {
+        const int64_t row = b0 + t;
+        if (row < 0 || row >= g_end - g_begin) continue;
+        const int e = c_runmask[start + t];
+        const double l = own[e], nb = nbs[e];
+        double tc, dtc, o;
+        if (et) {
+          tc = -0.5 * l - kd * e1 + ek;
+          dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
+          o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+        } else {
+          tc = -0.5 * l;
+          dtc = 0.5 * ((1.0 - kd) * l + nb);
+          o = 0.5 * ((kd - 2.0) * l - nb);
+        }
+        const int64_t oi = row * D + d;
+        __stcs(out + oi, tc);
+        __stcs(out + plane + oi, dtc);
+        __stcs(out + 2 * plane + oi, o);
+        __stcs(out + 3 * plane + oi, tc + dtc);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 void upload_tables() {
   static thread_local int uploaded_for = -1;
   int dev = 0;
@@ -425,6 +647,7 @@ void upload_tables() {
     lt[j].y = (double)(-logl((long double)cd));
   }
   cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * 256);
+  cudaMemcpyToSymbol(g_logtab, lt.data(), sizeof(double2) * 256);
   cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));
@@ -440,23 +663,71 @@ bool lattice_supports(int N) { return N >= CB + 2 && N <= MAXV; }
 int lattice_ws_bytes(int N, int D, size_t *bytes) {
   (void)D;
   if (!lattice_supports(N)) return fail(HOI_INVALID_ARG, "lattice engine needs 12 <= N <= 32");
-  *bytes = (sizeof(double) << N) + 4096;
+  // table 2^N f64 | misc (flag, err, counter, order offsets) 4 KB | flags 2^(N-10) u32
+  *bytes = (sizeof(double) << N) + 4096 + (sizeof(unsigned) << (N - CB));
   return HOI_OK;
 }
 
 // Workspace: [table 2^N doubles][flag int x16][order offsets int64 x33]
 struct LatticeWs {
   double *table;
-  int *flag;
-  int64_t *offs;
+  int *flag;          // phase-1 not-PD flag
+  int *err;           // fused pass: 1 not PD, 2 spin timeout
+  unsigned *counter;  // fused pass: block claim counter
+  int64_t *offs;      // order offsets
+  unsigned *ready;    // fused pass: per-block publish flags
 };
 
 static LatticeWs ws_view(void *ws, int N) {
   LatticeWs w;
+  char *base = reinterpret_cast<char *>(ws) + (sizeof(double) << N);
   w.table = reinterpret_cast<double *>(ws);
-  w.flag = reinterpret_cast<int *>(reinterpret_cast<char *>(ws) + (sizeof(double) << N));
-  w.offs = reinterpret_cast<int64_t *>(w.flag + 16);
+  w.flag = reinterpret_cast<int *>(base);
+  w.err = w.flag + 4;
+  w.counter = reinterpret_cast<unsigned *>(w.flag + 8);
+  w.offs = reinterpret_cast<int64_t *>(base + 64);
+  w.ready = reinterpret_cast<unsigned *>(base + 4096);
   return w;
+}
+
+int lattice_fused(const double *corr, int N, int D, int d, const double *eta, int kstride,
+                  int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, void *ws,
+                  size_t ws_bytes, cudaStream_t s) {
+  size_t need = 0;
+  int st = lattice_ws_bytes(N, D, &need);
+  if (st) return st;
+  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
+  upload_binomials();
+  upload_tables();
+  LatticeWs w = ws_view(ws, N);
+  const int nP = N - CB;
+  int64_t h_off[MAXV + 1];
+  int64_t acc = 0;
+  for (int k = kmin; k <= kmax; ++k) {
+    h_off[k - kmin] = acc;
+    acc += (int64_t)host_binom(N, k);
+  }
+  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(w.ready, 0, sizeof(unsigned) << nP, s);
+  cudaMemsetAsync(w.flag, 0, 64, s);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_fused, 32, 0);
+  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > (1ll << nP)) grid = 1ll << nP;
+  const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  k_lattice_fused<<<(unsigned)grid, 32, 0, s>>>(corr, N, D, d, kmin, kmax, eta, kstride, w.offs,
+                                                g_begin, g_end, out, plane, w.table, w.ready,
+                                                w.counter, w.err);
+  if ((st = check_launch("k_lattice_fused"))) return st;
+  int h_err = 0;
+  cudaMemcpyAsync(&h_err, w.err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  if (h_err == 1) return fail(HOI_FALLBACK, "lattice: correlation matrix not numerically positive "
+                                            "definite; rerun with the per-n-plet engine");
+  if (h_err) return fail(HOI_CUDA_ERROR, "lattice: fused pass timed out waiting for a block");
+  return HOI_OK;
 }
 
 int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_bytes,
@@ -517,9 +788,32 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
   return HOI_OK;
 }
 
+int scan_full_lattice_fused(const double *corr, const double *eta, int kstride, int N, int D,
+                            int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
+                            void *ws, size_t ws_bytes, cudaStream_t s) {
+  for (int d = 0; d < D; ++d) {
+    int st = lattice_fused(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
+                           ws_bytes, s);
+    if (st) return st;
+  }
+  return HOI_OK;
+}
+
 }  // namespace hoib
 
 using namespace hoib;
+
+extern "C" int hoi_lattice_fused(const double *corr, int32_t N, int32_t D, int32_t d,
+                                 const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
+                                 int64_t g_begin, int64_t g_end, double *out, void *ws,
+                                 size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && out && lattice_supports(N) && d >= 0 && d < D && kmin >= 1 &&
+                    kmin <= kmax && kmax <= N && g_begin >= 0 && g_begin <= g_end,
+                "hoi_lattice_fused: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_fused: bias table too short");
+  return lattice_fused(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
 
 extern "C" int hoi_lattice_table(const double *corr, int32_t N, int32_t D, int32_t d, void *ws,
                                  size_t ws_bytes, void *stream) {

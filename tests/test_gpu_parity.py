@@ -336,19 +336,20 @@ def _random_cov(n, seed):
     return r * np.outer(d, d)
 
 
+@pytest.mark.parametrize("engine", [2, 3])
 @pytest.mark.parametrize("n,lo,hi", [(12, 1, 12), (13, 2, 13), (16, 3, 9)])
 @pytest.mark.parametrize("bias", [False, True])
-def test_lattice_engine_vs_oracle(oracle, n, lo, hi, bias):
+def test_lattice_engine_vs_oracle(oracle, n, lo, hi, bias, engine):
     sig = _random_cov(n, n)
     sig = 0.5 * (sig + sig.T)
     covs = hoi.CovSet([hoi.CovarianceMatrix(sig, n_samples_used=500)])
-    dev = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=2)
+    dev = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=engine)
     _, vals = oracle.scan(sig, [500], lo, hi, oracle.CollectR(), bias=bias)
     np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
     # a sub-range of ranks lands at the same rows
     total = hoi.count_nplets(n, lo, hi)
     g0, g1 = total // 3, 2 * total // 3 + 1
-    part = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=2, g_begin=g0, g_end=g1)
+    part = hoi.scan_device(covs, lo, hi, bias_correct=bias, engine=engine, g_begin=g0, g_end=g1)
     np.testing.assert_array_equal(part.out.cpu().numpy(), dev.out[:, g0:g1].cpu().numpy())
 
 
@@ -361,6 +362,22 @@ def test_lattice_matches_percell_engine_cfg3(golden):
         err = (a - b).abs() - 1e-9 * b.abs()
         assert float(err.max()) <= 1e-11
         assert bool((a[3] == a[0] + a[1]).all())
+        # the fused single-pass engine computes the same table and stencil
+        c = hoi.scan_device(covs, 3, 20, bias_correct=bias, engine=3).out
+        err = (c - b).abs() - 1e-9 * b.abs()
+        assert float(err.max()) <= 1e-11
+
+
+def test_fused_lattice_cfg4_full(golden):
+    g = golden.npz("cfg4")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"], n_samples_used=int(g["t"]))])
+    out = hoi.scan_device(covs, 2, 30, engine=3).out
+    sel = torch.as_tensor(g["g"], device="cuda")
+    np.testing.assert_allclose(out[:, sel, :].cpu().numpy(), g["vals"], rtol=RTOL, atol=ATOL)
+    assert bool(torch.isfinite(out).all())
+    assert bool((out[3] == out[0] + out[1]).all())
+    del out
+    torch.cuda.empty_cache()
 
 
 def test_lattice_multi_dataset(oracle):
