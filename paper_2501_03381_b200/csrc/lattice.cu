@@ -52,6 +52,14 @@ __constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
 __constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
 __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
+// Global copies of the tables that are indexed per lane (constant memory
+// serialises divergent indices; these go through L1 with coalescing).
+__device__ uint16_t g_runmask[BLK];
+__device__ uint64_t g_binom[kBinomN * kBinomN];
+
+__device__ __forceinline__ uint64_t binom_g(int n, int m) {
+  return (m < 0 || n < 0 || m > n) ? 0ull : __ldg(g_binom + n * kBinomN + m);
+}
 
 __device__ __forceinline__ void lp_mul(double &m, int &e, double x) {
   m *= x;
@@ -275,11 +283,11 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const int q = tid, k = kP + q;
     int64_t base = -1;
     if (k >= kmin && k <= kmax && k >= 1) {
-      uint64_t r = binom(N, k) - 1;
+      uint64_t r = binom_g(N, k) - 1;
       int i = 0;
       for (int j = 0; j < nP; ++j)
-        if ((P >> j) & 1) r -= binom(N - 1 - j, k - i++);
-      for (int t = 0; t < q; ++t) r -= binom(N - 1 - (nP + t), k - i++);
+        if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
+      for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
       base = order_off[k - kmin] + (int64_t)r - g_begin;
     }
     s_base[q] = base;
@@ -362,7 +370,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     for (int t = tid; t < len; t += 256) {
       const int64_t row = b0 + t;
       if (row < 0 || row >= g_end - g_begin) continue;
-      const int e = c_runmask[start + t];
+      const int e = __ldg(g_runmask + start + t);
       const double l = own[e], nb = nbs[e];
       double tc, dtc, o;
       if (et) {
@@ -439,9 +447,10 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
     }
     __syncwarp();
     double *M = nbs;                                  // m <= 32 -> m*m <= 1024
-    for (int x = lane; x < m * m; x += 32) {
-      const int i = x / m, l = x - i * m;
-      M[x] = __ldg(corr + ((int64_t)vars[i] * N + vars[l]) * D + d);
+    if (lane < m) {
+      const int vl = vars[lane];
+      for (int i = 0; i < m; ++i)
+        M[i * m + lane] = __ldg(corr + ((int64_t)vars[i] * N + vl) * D + d);
     }
     __syncwarp();
     double m0 = 1.0;
@@ -452,10 +461,11 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
       bad |= !(p > kMinPivot);
       lp_mul(m0, e0, p);
       const double rp = 1.0 / p;
-      const int r = m - j - 1;
-      for (int x = lane; x < r * r; x += 32) {
-        const int i = j + 1 + x / r, l = j + 1 + x % r;
-        M[i * m + l] = fma(-M[i * m + j] * rp, M[j * m + l], M[i * m + l]);
+      // lane = column: row j's entry stays in a register, column j is a
+      // broadcast read, the lane's own column is conflict-free
+      if (lane > j && lane < m) {
+        const double mj = M[j * m + lane] * rp;
+        for (int i = j + 1; i < m; ++i) M[i * m + lane] = fma(-M[i * m + j], mj, M[i * m + lane]);
       }
       __syncwarp();
     }
@@ -549,11 +559,11 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
       const int q = lane, k = kP + q;
       int64_t base = -1;
       if (k >= kmin && k <= kmax && k >= 1) {
-        uint64_t r = binom(N, k) - 1;
+        uint64_t r = binom_g(N, k) - 1;
         int i = 0;
         for (int j = 0; j < nP; ++j)
-          if ((P >> j) & 1) r -= binom(N - 1 - j, k - i++);
-        for (int t = 0; t < q; ++t) r -= binom(N - 1 - (nP + t), k - i++);
+          if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
+        for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
         base = order_off[k - kmin] + (int64_t)r - g_begin;
       }
       s_base[q] = base;
@@ -584,7 +594,7 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
       for (int t = lane; t < len; t += 32) {
         const int64_t row = b0 + t;
         if (row < 0 || row >= g_end - g_begin) continue;
-        const int e = c_runmask[start + t];
+        const int e = __ldg(g_runmask + start + t);
         const double l = own[e], nb = nbs[e];
         double tc, dtc, o;
         if (et) {
@@ -648,6 +658,12 @@ void upload_tables() {
   }
   cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * 256);
   cudaMemcpyToSymbol(g_logtab, lt.data(), sizeof(double2) * 256);
+  cudaMemcpyToSymbol(g_runmask, rm.data(), sizeof(uint16_t) * BLK);
+  {
+    std::vector<uint64_t> hb(kBinomN * kBinomN);
+    fill_binomials(hb.data());
+    cudaMemcpyToSymbol(g_binom, hb.data(), sizeof(uint64_t) * hb.size());
+  }
   cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));

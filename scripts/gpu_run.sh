@@ -1,8 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest.log
-timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 300 python scripts/e2e_profile.py > gpurun_out/e2e_profile.log 2>&1
-timeout 1200 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
-nproc > gpurun_out/host.txt; lscpu | head -20 >> gpurun_out/host.txt
+python scripts/profile_target.py fused > gpurun_out/plain_fused.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lattice_fused -s 1 -c 1 -o gpurun_out/prof_fused python scripts/profile_target.py fused > gpurun_out/ncu_fused.log 2>&1
 echo done

@@ -20,9 +20,9 @@ from paper_2501_03381_b200.scanner import _ScanCtx  # noqa: E402
 
 def main(mode):
     _build.build()
-    if mode == "lattice":
+    if mode in ("lattice", "fused"):
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
-        ctx = _ScanCtx(covs, 2, 30, False, 2)
+        ctx = _ScanCtx(covs, 2, 30, False, 2 if mode == "lattice" else 3)
         total = hoi.count_nplets(30, 2, 30)
         out = torch.empty((4, total, 1), dtype=torch.float64, device="cuda")
         for _ in range(2):
