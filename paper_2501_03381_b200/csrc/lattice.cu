@@ -95,12 +95,19 @@ __device__ __forceinline__ double fast_log(double m, int e_extra, const double2 
   return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(r, p, t.y)));
 }
 
+// Shared-memory swizzle of a block's 1024 entries: the output pass reads
+// them in lexicographic-run order, which in mask order is a scatter with a
+// ~14-wavefront bank-conflict degree; XOR-ing the low 5 index bits with
+// the high 5 brings it to ~3.6 while neighbour/stencil and linear accesses
+// stay conflict-free (2 wavefronts per 8-byte warp access).
+__device__ __forceinline__ int swz(int e) { return (e & ~31) | ((e ^ (e >> 5)) & 31); }
+
 // Leaf recursion over the last R suffix variables held in registers as a
 // packed lower triangle.  Include/exclude variable 0 of the remainder; the
 // include branch takes the Schur complement.  2^R leaves, one log each.
 // The running pivot product m enters normalised to [0.5, 1) and picks up at
 // most R factors in [1e-12, 1], so it cannot underflow inside the recursion.
-template <int R>
+template <int R, bool SW>
 struct Leaf {
   static __device__ __forceinline__ void run(const double (&a)[R * (R + 1) / 2], double m, int e,
                                              int bits, double *__restrict__ out, int lane,
@@ -112,7 +119,7 @@ struct Leaf {
     for (int i = 1; i < R; ++i)
 #pragma unroll
       for (int l = 1; l <= i; ++l) ex[(i - 1) * i / 2 + (l - 1)] = a[i * (i + 1) / 2 + l];
-    Leaf<R1>::run(ex, m, e, bits, out, lane, bad, tab);
+    Leaf<R1, SW>::run(ex, m, e, bits, out, lane, bad, tab);
     // include: pivot a00, Schur complement of the rest
     const double p = a[0];
     bad |= !(p > kMinPivot);
@@ -125,17 +132,17 @@ struct Leaf {
       for (int l = 1; l <= i; ++l)
         in[(i - 1) * i / 2 + (l - 1)] = fma(-ai, a[l * (l + 1) / 2], a[i * (i + 1) / 2 + l]);
     }
-    Leaf<R1>::run(in, m * p, e, bits | (1 << (CB - R)), out, lane, bad, tab);
+    Leaf<R1, SW>::run(in, m * p, e, bits | (1 << (CB - R)), out, lane, bad, tab);
   }
 };
 
-template <>
-struct Leaf<0> {
+template <bool SW>
+struct Leaf<0, SW> {
   static __device__ __forceinline__ void run(const double (&)[1], double m, int e, int bits,
                                              double *__restrict__ out, int lane, int &,
                                              const double2 *__restrict__ tab) {
     // bits holds the F5..F9 pattern at bit positions 5..9
-    out[bits + lane] = fast_log(m, e, tab);
+    out[SW ? swz(bits + lane) : bits + lane] = fast_log(m, e, tab);
   }
 };
 
@@ -255,7 +262,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       ml = frexp(ml, &ex);
       el += ex;
     }
-    Leaf<R>::run(a, ml, el, 0, table + blk * BLK, lane, bad, s_logtab);
+    Leaf<R, false>::run(a, ml, el, 0, table + blk * BLK, lane, bad, s_logtab);
     if (bad) s_bad = 1;
   }
   __syncthreads();
@@ -302,55 +309,59 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
   }
   if (!any) return;
-  // Thread tid owns entries {2tid, 2tid+1, 512+2tid, 513+2tid} (16-byte loads).
-  // Neighbour blocks along the low block bits were touched a few thousand
-  // CTAs earlier and are served from L2 (ld.cg); blocks along the top
-  // kFarBits bits were not, so they are streamed with evict-first loads
-  // (ld.cs) instead of displacing the reusable near window.
-  const double2 *tb = reinterpret_cast<const double2 *>(table + P * BLK);
-  const double2 o0 = __ldcg(tb + tid), o1 = __ldcg(tb + 256 + tid);
-  reinterpret_cast<double2 *>(own)[tid] = o0;
-  reinterpret_cast<double2 *>(own)[256 + tid] = o1;
-  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  // Thread tid owns entries e = tid + 256 r (coalesced 8-byte loads; the
+  // stencil's shared-memory reads are then conflict-free).  Neighbour blocks
+  // along the low block bits were touched a few thousand CTAs earlier and are
+  // served from L2 (ld.cg); blocks along the top kFarBits bits were not, so
+  // they are streamed with evict-first loads (ld.cs) instead of displacing
+  // the reusable near window.  own/nbs are stored swizzled (swz).
+  const double *tb = table + P * BLK;
+  double acc[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    own[swz(tid + 256 * r)] = __ldcg(tb + tid + 256 * r);
+    acc[r] = 0.0;
+  }
   const int near_bits = nP > kFarBits + kMinNearBits ? nP - kFarBits : nP;
   const uint32_t near_mask = (1u << near_bits) - 1u;
   uint32_t near = (uint32_t)P & near_mask, far = (uint32_t)P & ~near_mask;
   while (near) {
     const int j0 = __ffs(near) - 1;
     near &= near - 1;
-    const double2 *n0 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j0)) * BLK);
-    const double2 x0 = __ldcg(n0 + tid), y0 = __ldcg(n0 + 256 + tid);
+    const double *n0 = table + (P ^ (1ll << j0)) * BLK;
+    double x0[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) x0[r] = __ldcg(n0 + tid + 256 * r);
     if (near) {
       const int j1 = __ffs(near) - 1;
       near &= near - 1;
-      const double2 *n1 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j1)) * BLK);
-      const double2 x1 = __ldcg(n1 + tid), y1 = __ldcg(n1 + 256 + tid);
-      a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
-      a0.x += x1.x; a0.y += x1.y; a1.x += y1.x; a1.y += y1.y;
+      const double *n1 = table + (P ^ (1ll << j1)) * BLK;
+      double x1[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) x1[r] = __ldcg(n1 + tid + 256 * r);
+#pragma unroll
+      for (int r = 0; r < PER; ++r) acc[r] += x0[r] + x1[r];
     } else {
-      a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) acc[r] += x0[r];
     }
   }
   while (far) {
     const int j0 = __ffs(far) - 1;
     far &= far - 1;
-    const double2 *n0 = reinterpret_cast<const double2 *>(table + (P ^ (1ll << j0)) * BLK);
-    const double2 x0 = __ldcs(n0 + tid), y0 = __ldcs(n0 + 256 + tid);
-    a0.x += x0.x; a0.y += x0.y; a1.x += y0.x; a1.y += y0.y;
+    const double *n0 = table + (P ^ (1ll << j0)) * BLK;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) acc[r] += __ldcs(n0 + tid + 256 * r);
   }
   __syncthreads();
-  {
-    const int es[4] = {2 * tid, 2 * tid + 1, 512 + 2 * tid, 513 + 2 * tid};
-    const double as[4] = {a0.x, a0.y, a1.x, a1.y};
 #pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const int e = es[r];
-      double s = as[r];
+  for (int r = 0; r < PER; ++r) {
+    const int e = tid + 256 * r;
+    double s = acc[r];
 #pragma unroll
-      for (int t = 0; t < CB; ++t)
-        if ((e >> t) & 1) s += own[e ^ (1 << t)];
-      nbs[e] = s;
-    }
+    for (int t = 0; t < CB; ++t)
+      if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
+    nbs[swz(e)] = s;
   }
   __syncthreads();
   const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
@@ -371,7 +382,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       const int64_t row = b0 + t;
       if (row < 0 || row >= g_end - g_begin) continue;
       const int e = __ldg(g_runmask + start + t);
-      const double l = own[e], nb = nbs[e];
+      const double l = own[swz(e)], nb = nbs[swz(e)];
       double tc, dtc, o;
       if (et) {
         tc = -0.5 * l - kd * e1 + ek;
@@ -503,24 +514,23 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
 #pragma unroll
       for (int l = 0; l <= i; ++l)
         a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
-    Leaf<R>::run(a, ml, el, 0, own, lane, bad, logtab);
+    Leaf<R, true>::run(a, ml, el, 0, own, lane, bad, logtab);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
     __syncwarp();
     // publish: table block to HBM (kept in L2 for the near consumers)
     {
-      const double2 *o2 = reinterpret_cast<const double2 *>(own);
-      double2 *t2 = reinterpret_cast<double2 *>(table + (int64_t)P * BLK);
-#pragma unroll 4
-      for (int x = lane; x < BLK / 2; x += 32) __stcg(t2 + x, o2[x]);
+      double *tp = table + (int64_t)P * BLK;
+#pragma unroll 8
+      for (int x = 0; x < BLK / 32; ++x) __stcg(tp + 32 * x + lane, own[swz(32 * x + lane)]);
     }
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(flags + P, 1u);
     // ------------------------------------------------ consume P ------
-    // lane owns entries e = 64 x + 2 lane + {0,1}, x = 0..15
-    double2 acc[BLK / 64];
+    // lane owns entries e = 32 x + lane, x = 0..31
+    double acc[BLK / 32];
 #pragma unroll
-    for (int x = 0; x < BLK / 64; ++x) acc[x] = make_double2(0.0, 0.0);
+    for (int x = 0; x < BLK / 32; ++x) acc[x] = 0.0;
     uint32_t rem = P;
     while (rem) {
       const int j = 31 - __clz(rem);                 // far (high) bits first
@@ -536,21 +546,13 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
         }
       }
       __syncwarp();
-      const double2 *nb = reinterpret_cast<const double2 *>(table + (int64_t)Pn * BLK);
+      const double *nb = table + (int64_t)Pn * BLK;
       if (j >= near_bits) {
 #pragma unroll
-        for (int x = 0; x < BLK / 64; ++x) {
-          const double2 v = __ldcs(nb + 32 * x + lane);
-          acc[x].x += v.x;
-          acc[x].y += v.y;
-        }
+        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcs(nb + 32 * x + lane);
       } else {
 #pragma unroll
-        for (int x = 0; x < BLK / 64; ++x) {
-          const double2 v = __ldcg(nb + 32 * x + lane);
-          acc[x].x += v.x;
-          acc[x].y += v.y;
-        }
+        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcg(nb + 32 * x + lane);
       }
     }
     // lexicographic base rank of each run
@@ -569,16 +571,13 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
       s_base[q] = base;
     }
 #pragma unroll
-    for (int x = 0; x < BLK / 64; ++x) {
+    for (int x = 0; x < BLK / 32; ++x) {
+      const int e = 32 * x + lane;
+      double s = acc[x];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = 64 * x + 2 * lane + h;
-        double s = h ? acc[x].y : acc[x].x;
-#pragma unroll
-        for (int t = 0; t < CB; ++t)
-          if ((e >> t) & 1) s += own[e ^ (1 << t)];
-        nbs[e] = s;
-      }
+      for (int t = 0; t < CB; ++t)
+        if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
+      nbs[swz(e)] = s;
     }
     __syncwarp();
     const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
@@ -595,7 +594,7 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
         const int64_t row = b0 + t;
         if (row < 0 || row >= g_end - g_begin) continue;
         const int e = __ldg(g_runmask + start + t);
-        const double l = own[e], nb = nbs[e];
+        const double l = own[swz(e)], nb = nbs[swz(e)];
         double tc, dtc, o;
         if (et) {
           tc = -0.5 * l - kd * e1 + ek;
