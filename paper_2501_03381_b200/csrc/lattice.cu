@@ -151,7 +151,8 @@ struct Leaf<0, SW> {
 // lane of a warp owns one pattern of F0..F4 and recurses over F5..F9.
 __global__ void __launch_bounds__(256, 2)
 k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
-                double *__restrict__ table, int *__restrict__ flag) {
+                double *__restrict__ table, int *__restrict__ flag, unsigned cta_off) {
+  const unsigned cta = blockIdx.x + cta_off;
   __shared__ double2 s_logtab[256];
   constexpr int MS = MAXV + 1;
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
@@ -167,7 +168,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
-      if ((blockIdx.x >> (j - b)) & 1) vars[nf++] = j;
+      if ((cta >> (j - b)) & 1) vars[nf++] = j;
     s_nfix = nf;
     for (int j = 0; j < b; ++j) vars[nf + j] = j;
     for (int t = 0; t < CB; ++t) vars[nf + b + t] = nP + t;
@@ -256,7 +257,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
 #pragma unroll
       for (int l = 0; l <= i; ++l)
         a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
-    const int64_t blk = ((int64_t)blockIdx.x << b) | u;
+    const int64_t blk = ((int64_t)cta << b) | u;
     {
       int ex;
       ml = frexp(ml, &ex);
@@ -276,17 +277,19 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
 __global__ void __launch_bounds__(256)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
-                   int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane) {
+                   int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
+                   int64_t blk_off, int near_bits, int partial) {
   __shared__ double own[BLK];
   __shared__ double nbs[BLK];
   __shared__ int64_t s_base[CB + 1];
   constexpr int PER = BLK / 256;
   const int tid = threadIdx.x;
-  const int64_t P = blockIdx.x;
+  const int64_t P = (int64_t)blockIdx.x + blk_off;
   const int kP = __popcll(P);
   const int nP = N - CB;
-  // lexicographic base rank of each run (P u {first q suffix variables})
-  if (tid <= CB) {
+  // lexicographic base rank of each run (P u {first q suffix variables});
+  // a full-range pass computes it after issuing the table loads (below)
+  if (partial && tid <= CB) {
     const int q = tid, k = kP + q;
     int64_t base = -1;
     if (k >= kmin && k <= kmax && k >= 1) {
@@ -299,16 +302,18 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     }
     s_base[q] = base;
   }
-  __syncthreads();
-  // skip blocks with no output in [g_begin, g_end)
-  bool any = false;
-  for (int q = 0; q <= CB; ++q) {
-    int64_t b0 = s_base[q];
-    if (kP + q < kmin || kP + q > kmax || kP + q < 1) continue;
-    int64_t len = (int64_t)binom(CB, q);
-    if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
+  if (partial) {
+    __syncthreads();
+    // skip blocks with no output in [g_begin, g_end)
+    bool any = false;
+    for (int q = 0; q <= CB; ++q) {
+      int64_t b0 = s_base[q];
+      if (kP + q < kmin || kP + q > kmax || kP + q < 1) continue;
+      int64_t len = (int64_t)binom(CB, q);
+      if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
+    }
+    if (!any) return;
   }
-  if (!any) return;
   // Thread tid owns entries e = tid + 256 r (coalesced 8-byte loads; the
   // stencil's shared-memory reads are then conflict-free).  Neighbour blocks
   // along the low block bits were touched a few thousand CTAs earlier and are
@@ -316,13 +321,12 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   // they are streamed with evict-first loads (ld.cs) instead of displacing
   // the reusable near window.  own/nbs are stored swizzled (swz).
   const double *tb = table + P * BLK;
-  double acc[PER];
+  double acc[PER], ov[PER];
 #pragma unroll
   for (int r = 0; r < PER; ++r) {
-    own[swz(tid + 256 * r)] = __ldcg(tb + tid + 256 * r);
-    acc[r] = 0.0;
+    ov[r] = __ldcg(tb + tid + 256 * r);       // stored to shared memory after the
+    acc[r] = 0.0;                             // neighbour loads have been issued
   }
-  const int near_bits = nP > kFarBits + kMinNearBits ? nP - kFarBits : nP;
   const uint32_t near_mask = (1u << near_bits) - 1u;
   uint32_t near = (uint32_t)P & near_mask, far = (uint32_t)P & ~near_mask;
   while (near) {
@@ -352,6 +356,21 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const double *n0 = table + (P ^ (1ll << j0)) * BLK;
 #pragma unroll
     for (int r = 0; r < PER; ++r) acc[r] += __ldcs(n0 + tid + 256 * r);
+  }
+#pragma unroll
+  for (int r = 0; r < PER; ++r) own[swz(tid + 256 * r)] = ov[r];
+  if (!partial && tid <= CB) {
+    const int q = tid, k = kP + q;
+    int64_t base = -1;
+    if (k >= kmin && k <= kmax && k >= 1) {
+      uint64_t r = binom_g(N, k) - 1;
+      int i = 0;
+      for (int j = 0; j < nP; ++j)
+        if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
+      for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
+      base = order_off[k - kmin] + (int64_t)r - g_begin;
+    }
+    s_base[q] = base;
   }
   __syncthreads();
 #pragma unroll
@@ -756,8 +775,19 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
-  k_lattice_table<<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag);
+  k_lattice_table<<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag, 0u);
   return check_launch("k_lattice_table");
+}
+
+static int default_near_bits(int nP) { return nP > kFarBits + kMinNearBits ? nP - kFarBits : nP; }
+
+static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
+  int64_t acc = 0;
+  for (int k = kmin; k <= kmax; ++k) {
+    h_off[k - kmin] = acc;
+    acc += (int64_t)host_binom(N, k);
+  }
+  return acc;
 }
 
 int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
@@ -766,16 +796,77 @@ int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstri
   upload_tables();
   LatticeWs w = ws_view(ws, N);
   int64_t h_off[MAXV + 1];
-  int64_t acc = 0;
-  for (int k = kmin; k <= kmax; ++k) {
-    h_off[k - kmin] = acc;
-    acc += (int64_t)host_binom(N, k);
-  }
+  const int64_t total = total_rows(N, kmin, kmax, h_off);
   cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
   const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  const int partial = (g_begin > 0 || g_end < total) ? 1 : 0;
   k_lattice_measures<<<1u << (N - CB), 256, 0, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
-                                                    w.offs, g_begin, g_end, out, plane);
+                                                    w.offs, g_begin, g_end, out, plane, 0,
+                                                    default_near_bits(N - CB), partial);
   return check_launch("k_lattice_measures");
+}
+
+// Two-stream pipeline over chunks of 2^w table blocks: the table of chunk
+// c+1 is built on an auxiliary stream while the stencil consumes chunk c,
+// so a chunk's own blocks and its neighbours within distance 2^w (the
+// current and previous chunk, 2 x 64 MB) are read from L2 while hot, and
+// the FP64/log-bound table phase overlaps the HBM-bound stencil.
+struct PipeRes {
+  int dev = -1;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev[1 << 10];
+  int nev = 0;
+};
+
+static PipeRes &pipe_res(int nev) {
+  static thread_local PipeRes r;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (r.dev != dev) {
+    r = PipeRes();
+    r.dev = dev;
+    cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking);
+  }
+  while (r.nev < nev) cudaEventCreateWithFlags(&r.ev[r.nev++], cudaEventDisableTiming);
+  return r;
+}
+
+int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta, int kstride,
+                     int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, void *ws,
+                     size_t ws_bytes, cudaStream_t s) {
+  size_t need = 0;
+  int st = lattice_ws_bytes(N, D, &need);
+  if (st) return st;
+  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
+  upload_binomials();
+  upload_tables();
+  LatticeWs w = ws_view(ws, N);
+  const int nP = N - CB;
+  const int b = nP < MAXB ? nP : MAXB;
+  const int wb = nP < 13 ? nP : 13;                 // chunk = 2^wb blocks (64 MB of table)
+  const int nchunks = 1 << (nP - wb);
+  int64_t h_off[MAXV + 1];
+  const int64_t total = total_rows(N, kmin, kmax, h_off);
+  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+  PipeRes &pr = pipe_res(nchunks + 1);
+  cudaEventRecord(pr.ev[nchunks], s);
+  cudaStreamWaitEvent(pr.aux, pr.ev[nchunks], 0);
+  const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  const int partial = (g_begin > 0 || g_end < total) ? 1 : 0;
+  const int near_bits = wb + 1 < nP ? wb + 1 : nP;   // neighbours in this or the previous chunk
+  const unsigned ctas = 1u << (wb - b);
+  for (int c = 0; c < nchunks; ++c) {
+    k_lattice_table<<<ctas, 256, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
+    if ((st = check_launch("k_lattice_table"))) return st;
+    cudaEventRecord(pr.ev[c], pr.aux);
+    cudaStreamWaitEvent(s, pr.ev[c], 0);
+    k_lattice_measures<<<1u << wb, 256, 0, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
+                                                w.offs, g_begin, g_end, out, plane,
+                                                (int64_t)c << wb, near_bits, partial);
+    if ((st = check_launch("k_lattice_measures"))) return st;
+  }
+  return HOI_OK;
 }
 
 int lattice_status(void *ws, int N, cudaStream_t s) {
@@ -793,12 +884,11 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
                       void *ws, size_t ws_bytes, cudaStream_t s) {
   (void)err_count;
   for (int d = 0; d < D; ++d) {
-    int st = lattice_table(corr, N, D, d, ws, ws_bytes, s);
+    int st = lattice_pipeline(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
+                              ws_bytes, s);
     if (st) return st;
-    st = lattice_status(ws, N, s);
-    if (st) return st;
-    st = lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, s);
-    if (st) return st;
+    st = lattice_status(ws, N, s);      // rows written from a flagged table are redone
+    if (st) return st;                  // by the caller with engine 1 (HOI_FALLBACK)
   }
   return HOI_OK;
 }

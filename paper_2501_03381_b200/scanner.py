@@ -337,19 +337,11 @@ class _ScanCtx:
             out = torch.empty((4, rows, self.d), dtype=torch.float64, device="cuda")
         cnt, coords = _err_buffers(torch)
         s = nat.stream_handle(torch)
-        if self.engine == 2 and self.d == 1:
-            rc = nat.OK
-            if not (reuse_table and getattr(self, "_table_ok", False)):
-                self._table_ok = False
-                rc = lib.hoi_lattice_table(self.st.corr.data_ptr(), self.n, 1, 0,
-                                           self.ws.data_ptr(), self.ws.numel(), s)
-                if rc == nat.OK:
-                    rc = lib.hoi_lattice_status(self.ws.data_ptr(), self.n, s)
-                self._table_ok = rc == nat.OK
-            if rc == nat.OK:
-                kst = 0 if self.eta is None else self.eta.shape[1]
-                rc = lib.hoi_lattice_measures(self.ws.data_ptr(), self.n, 1, 0, nat.ptr(self.eta),
-                                              kst, self.lo, self.hi, g0, g1, out.data_ptr(), s)
+        if self.engine == 2 and self.d == 1 and reuse_table and getattr(self, "_table_ok", False):
+            # the log-det table of an earlier chunk of this scan is complete
+            kst = 0 if self.eta is None else self.eta.shape[1]
+            rc = lib.hoi_lattice_measures(self.ws.data_ptr(), self.n, 1, 0, nat.ptr(self.eta),
+                                          kst, self.lo, self.hi, g0, g1, out.data_ptr(), s)
         else:
             rc = lib.hoi_scan_full(*self._args(g0, g1), out.data_ptr(), cnt.data_ptr(),
                                    coords.data_ptr(), ERR_CAP, self.ws.data_ptr(),
@@ -362,6 +354,8 @@ class _ScanCtx:
             self._alloc_ws()
             return self.full(g0, g1, out)
         nat.check(rc, "scan_full")
+        # after a full engine-2 pass (D == 1) the workspace holds the whole table
+        self._table_ok = self.engine == 2 and self.d == 1
         return out, cnt, coords
 
 
