@@ -263,33 +263,82 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       ml = frexp(ml, &ex);
       el += ex;
     }
-    Leaf<R, false>::run(a, ml, el, 0, table + blk * BLK, lane, bad, s_logtab);
+    Leaf<R, true>::run(a, ml, el, 0, table + blk * BLK, lane, bad, s_logtab);   // swizzled
     if (bad) s_bad = 1;
   }
   __syncthreads();
   if (tid == 0 && s_bad) atomicExch(flag, 1);
 }
 
-// Phase 2: one CTA per table block P.  Sums the leave-one-out neighbours
-// (the |P| neighbour blocks streamed from L2/HBM plus the in-block
-// neighbours from shared memory), forms the four measures and writes each
-// order's run at its lexicographic output position.
+// TMA bulk-copy / mbarrier helpers (the sm_90+/sm_100 bulk copy engine).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
+  uint64_t p;
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+constexpr int kStages = 4;
+
+// Phase 2: one CTA per table block P.  The table is stored swizzled (swz),
+// so whole 8 KB blocks move HBM/L2 -> shared memory with TMA bulk copies:
+// the own block plus a kStages-deep ring of neighbour blocks (far ones first,
+// evict-first; near ones from L2), summed as they land.  In-block
+// neighbours come from shared memory; the four measures are written as
+// each order's lexicographic run.
 __global__ void __launch_bounds__(256)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
                    int64_t blk_off, int near_bits, int partial) {
-  __shared__ double own[BLK];
-  __shared__ double nbs[BLK];
+  __shared__ __align__(128) double own[BLK];
+  __shared__ __align__(128) double ring[kStages][BLK];
+  __shared__ __align__(8) uint64_t bars[kStages + 1];
   __shared__ int64_t s_base[CB + 1];
+  __shared__ unsigned s_nb[MAXV];
+  __shared__ int s_cnt;
+  double *nbs = ring[0];                 // reused once every neighbour is consumed
   constexpr int PER = BLK / 256;
+  constexpr uint32_t kBlkBytes = BLK * sizeof(double);
   const int tid = threadIdx.x;
   const int64_t P = (int64_t)blockIdx.x + blk_off;
   const int kP = __popcll(P);
   const int nP = N - CB;
-  // lexicographic base rank of each run (P u {first q suffix variables});
-  // a full-range pass computes it after issuing the table loads (below)
-  if (partial && tid <= CB) {
+  // lexicographic base rank of each run (P u {first q suffix variables})
+  if (tid <= CB) {
     const int q = tid, k = kP + q;
     int64_t base = -1;
     if (k >= kmin && k <= kmax && k >= 1) {
@@ -302,9 +351,17 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     }
     s_base[q] = base;
   }
+  if (tid == 32) {
+    for (int s = 0; s <= kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    int c = 0;
+    for (int j = nP - 1; j >= 0; --j)          // far (high) bits first
+      if ((P >> j) & 1) s_nb[c++] = (unsigned)(P ^ (1ll << j));
+    s_cnt = c;
+  }
+  __syncthreads();
   if (partial) {
-    __syncthreads();
-    // skip blocks with no output in [g_begin, g_end)
+    // skip blocks with no output in [g_begin, g_end) (before any copy is issued)
     bool any = false;
     for (int q = 0; q <= CB; ++q) {
       int64_t b0 = s_base[q];
@@ -314,65 +371,36 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     }
     if (!any) return;
   }
-  // Thread tid owns entries e = tid + 256 r (coalesced 8-byte loads; the
-  // stencil's shared-memory reads are then conflict-free).  Neighbour blocks
-  // along the low block bits were touched a few thousand CTAs earlier and are
-  // served from L2 (ld.cg); blocks along the top kFarBits bits were not, so
-  // they are streamed with evict-first loads (ld.cs) instead of displacing
-  // the reusable near window.  own/nbs are stored swizzled (swz).
-  const double *tb = table + P * BLK;
-  double acc[PER], ov[PER];
-#pragma unroll
-  for (int r = 0; r < PER; ++r) {
-    ov[r] = __ldcg(tb + tid + 256 * r);       // stored to shared memory after the
-    acc[r] = 0.0;                             // neighbour loads have been issued
-  }
-  const uint32_t near_mask = (1u << near_bits) - 1u;
-  uint32_t near = (uint32_t)P & near_mask, far = (uint32_t)P & ~near_mask;
-  while (near) {
-    const int j0 = __ffs(near) - 1;
-    near &= near - 1;
-    const double *n0 = table + (P ^ (1ll << j0)) * BLK;
-    double x0[PER];
-#pragma unroll
-    for (int r = 0; r < PER; ++r) x0[r] = __ldcg(n0 + tid + 256 * r);
-    if (near) {
-      const int j1 = __ffs(near) - 1;
-      near &= near - 1;
-      const double *n1 = table + (P ^ (1ll << j1)) * BLK;
-      double x1[PER];
-#pragma unroll
-      for (int r = 0; r < PER; ++r) x1[r] = __ldcg(n1 + tid + 256 * r);
-#pragma unroll
-      for (int r = 0; r < PER; ++r) acc[r] += x0[r] + x1[r];
-    } else {
-#pragma unroll
-      for (int r = 0; r < PER; ++r) acc[r] += x0[r];
+  const int cnt = s_cnt;
+  if (tid == 32) {
+    const uint64_t pol_own = l2_policy(false);
+    mbar_expect_tx(&bars[kStages], kBlkBytes);
+    tma_load_1d(own, table + P * BLK, kBlkBytes, &bars[kStages], pol_own);
+    for (int i = 0; i < cnt && i < kStages; ++i) {
+      const unsigned nb = s_nb[i];
+      const bool far = ((P ^ (int64_t)nb) >> near_bits) != 0;
+      mbar_expect_tx(&bars[i], kBlkBytes);
+      tma_load_1d(ring[i], table + (int64_t)nb * BLK, kBlkBytes, &bars[i], l2_policy(far));
     }
   }
-  while (far) {
-    const int j0 = __ffs(far) - 1;
-    far &= far - 1;
-    const double *n0 = table + (P ^ (1ll << j0)) * BLK;
+  double acc[PER];
 #pragma unroll
-    for (int r = 0; r < PER; ++r) acc[r] += __ldcs(n0 + tid + 256 * r);
-  }
+  for (int r = 0; r < PER; ++r) acc[r] = 0.0;
+  for (int i = 0; i < cnt; ++i) {
+    const int st = i % kStages;
+    mbar_wait(&bars[st], (uint32_t)((i / kStages) & 1));
 #pragma unroll
-  for (int r = 0; r < PER; ++r) own[swz(tid + 256 * r)] = ov[r];
-  if (!partial && tid <= CB) {
-    const int q = tid, k = kP + q;
-    int64_t base = -1;
-    if (k >= kmin && k <= kmax && k >= 1) {
-      uint64_t r = binom_g(N, k) - 1;
-      int i = 0;
-      for (int j = 0; j < nP; ++j)
-        if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
-      for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
-      base = order_off[k - kmin] + (int64_t)r - g_begin;
+    for (int r = 0; r < PER; ++r) acc[r] += ring[st][swz(tid + 256 * r)];
+    __syncthreads();                             // stage consumed by every thread
+    if (tid == 32 && i + kStages < cnt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const unsigned nb = s_nb[i + kStages];
+      const bool far = ((P ^ (int64_t)nb) >> near_bits) != 0;
+      mbar_expect_tx(&bars[st], kBlkBytes);
+      tma_load_1d(ring[st], table + (int64_t)nb * BLK, kBlkBytes, &bars[st], l2_policy(far));
     }
-    s_base[q] = base;
   }
-  __syncthreads();
+  mbar_wait(&bars[kStages], 0);
 #pragma unroll
   for (int r = 0; r < PER; ++r) {
     const int e = tid + 256 * r;
@@ -540,7 +568,7 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
     {
       double *tp = table + (int64_t)P * BLK;
 #pragma unroll 8
-      for (int x = 0; x < BLK / 32; ++x) __stcg(tp + 32 * x + lane, own[swz(32 * x + lane)]);
+      for (int x = 0; x < BLK / 32; ++x) __stcg(tp + 32 * x + lane, own[32 * x + lane]);
     }
     __threadfence();
     __syncwarp();
@@ -568,10 +596,10 @@ k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, 
       const double *nb = table + (int64_t)Pn * BLK;
       if (j >= near_bits) {
 #pragma unroll
-        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcs(nb + 32 * x + lane);
+        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcs(nb + swz(32 * x + lane));
       } else {
 #pragma unroll
-        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcg(nb + 32 * x + lane);
+        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcg(nb + swz(32 * x + lane));
       }
     }
     // lexicographic base rank of each run
