@@ -311,127 +311,212 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
-constexpr int kStages = 4;
+constexpr int kRing = 6;            // 8 KB table blocks in flight per CTA
+constexpr int kConsumerWarps = 8;
+constexpr int kStencilThreads = 32 * kConsumerWarps;   // consumers; + 1 producer warp
+constexpr int PER = BLK / kStencilThreads;
 
-// Phase 2: one CTA per table block P.  The table is stored swizzled (swz),
-// so whole 8 KB blocks move HBM/L2 -> shared memory with TMA bulk copies:
-// the own block plus a kStages-deep ring of neighbour blocks (far ones first,
-// evict-first; near ones from L2), summed as they land.  In-block
-// neighbours come from shared memory; the four measures are written as
-// each order's lexicographic run.
-__global__ void __launch_bounds__(256)
+// Dynamic shared memory of the stencil kernel.
+struct StencilSmem {
+  double ring[kRing][BLK];           // TMA destination ring (48 KB)
+  double nbs[2][BLK];                // sum of the k leave-one-out log-dets per entry
+  uint32_t run[BLK];                 // run position p -> e | lexrank << 10 | q << 20
+  uint64_t full[kRing];              // TMA landed
+  uint64_t empty[kRing];             // every consumer warp is done with the slot
+  int64_t base[2][CB + 1];           // output row of the first n-plet of run q
+};
+
+// Lexicographic rank contributions that depend only on the run length q:
+// the n-plet P u {first q suffix variables} has rank
+//   C(N,k) - 1 - sum_i C(N-1-p_i, k-i) - sum_{t<q} C(CB-1-t, q-t)
+// (unranking identity of ref nplet_engine.py:128-136's lexicographic order).
+__constant__ uint64_t c_suffix_term[CB + 1];
+
+constexpr int64_t kNoRun = INT64_MIN;
+
+// Output row (relative to g_begin) of P u {first q suffix variables}, or
+// kNoRun when its order is outside [kmin, kmax].  Every binomial load is
+// independent (fixed unrolled loop, predicated), so one L1 latency.
+__device__ __forceinline__ int64_t run_base(unsigned P, int q, int N, int kmin, int kmax,
+                                            const int64_t *__restrict__ order_off,
+                                            int64_t g_begin) {
+  const int nP = N - CB;
+  const int k = __popc(P) + q;
+  if (k < kmin || k > kmax || k < 1) return kNoRun;
+  uint64_t a = 0;
+#pragma unroll
+  for (int j = 0; j < MAXV - CB; ++j) {
+    const bool on = j < nP && ((P >> j) & 1u);
+    const int i = __popc(P & ((1u << j) - 1u));
+    a += on ? binom_g(N - 1 - j, k - i) : 0ull;
+  }
+  const uint64_t r = binom_g(N, k) - 1ull - a - c_suffix_term[q];
+  return order_off[k - kmin] + (int64_t)r - g_begin;
+}
+
+// 1 if table block P has at least one output row in [g_begin, g_end).
+__global__ void k_block_active(int N, int kmin, int kmax, const int64_t *__restrict__ order_off,
+                               int64_t g_begin, int64_t g_end, unsigned nblocks,
+                               uint8_t *__restrict__ active) {
+  const unsigned P = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P >= nblocks) return;
+  bool any = false;
+  for (int q = 0; q <= CB; ++q) {
+    const int64_t b0 = run_base(P, q, N, kmin, kmax, order_off, g_begin);
+    if (b0 == kNoRun) continue;
+    const int64_t len = (int64_t)binom(CB, q);
+    if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
+  }
+  active[P] = any ? 1 : 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr unsigned kEndBlock = 0xFFFFFFFFu;
+constexpr int kBlkQ = 16;              // > blocks the producer can run ahead (kRing + 1)
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Phase 2 (persistent, warp-specialised).  Warp 8 is the producer: one lane
+// claims table blocks from a global counter in increasing order (dynamic
+// claiming keeps the processing front a few hundred blocks wide, so a
+// neighbour block T[P ^ 2^j] below the L2 window is still L2-resident when
+// read; static strided assignment lets CTAs drift apart by thousands of
+// blocks and doubled DRAM reads) and streams, per block, the neighbour
+// blocks T[P \ j] (far bits first, evict-first beyond the L2 window) and
+// then the own block T[P] as 8 KB TMA bulk copies into a kRing-deep ring
+// guarded by full/empty mbarriers.  The ring never drains between blocks, so
+// the next block's neighbours stream in while this block's stencil and
+// epilogue run.  Warps 0-7 consume: each thread accumulates its 4 entries
+// from every neighbour slot and releases it (one arrival per warp, no
+// CTA-wide barrier), adds the in-block neighbours from the own block, and --
+// after the only per-block barrier (named, consumers only; nbs/base are
+// double-buffered) -- writes the four measures of each run (P, q) as one
+// coalesced, contiguous span of the order-major lexicographic output.
+__global__ void __launch_bounds__(kStencilThreads + 32, 3)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
-                   int64_t blk_off, int near_bits, int partial) {
-  __shared__ __align__(128) double own[BLK];
-  __shared__ __align__(128) double ring[kStages][BLK];
-  __shared__ __align__(8) uint64_t bars[kStages + 1];
-  __shared__ int64_t s_base[CB + 1];
-  __shared__ unsigned s_nb[MAXV];
-  __shared__ int s_cnt;
-  double *nbs = ring[0];                 // reused once every neighbour is consumed
-  constexpr int PER = BLK / 256;
+                   unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
+                   int near_bits, unsigned *__restrict__ counter) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StencilSmem &sm = *reinterpret_cast<StencilSmem *>(smem_raw);
+  __shared__ unsigned blkq[kBlkQ];
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
-  const int tid = threadIdx.x;
-  const int64_t P = (int64_t)blockIdx.x + blk_off;
-  const int kP = __popcll(P);
-  const int nP = N - CB;
-  // lexicographic base rank of each run (P u {first q suffix variables})
-  if (tid <= CB) {
-    const int q = tid, k = kP + q;
-    int64_t base = -1;
-    if (k >= kmin && k <= kmax && k >= 1) {
-      uint64_t r = binom_g(N, k) - 1;
-      int i = 0;
-      for (int j = 0; j < nP; ++j)
-        if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
-      for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
-      base = order_off[k - kmin] + (int64_t)r - g_begin;
-    }
-    s_base[q] = base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int p = tid; p < BLK; p += blockDim.x) {
+    const int e = __ldg(g_runmask + p);
+    const int q = __popc(e);
+    sm.run[p] = (uint32_t)e | ((uint32_t)(p - c_runstart[q]) << 10) | ((uint32_t)q << 20);
   }
-  if (tid == 32) {
-    for (int s = 0; s <= kStages; ++s) mbar_init(&bars[s], 1);
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    int c = 0;
-    for (int j = nP - 1; j >= 0; --j)          // far (high) bits first
-      if ((P >> j) & 1) s_nb[c++] = (unsigned)(P ^ (1ll << j));
-    s_cnt = c;
   }
   __syncthreads();
-  if (partial) {
-    // skip blocks with no output in [g_begin, g_end) (before any copy is issued)
-    bool any = false;
-    for (int q = 0; q <= CB; ++q) {
-      int64_t b0 = s_base[q];
-      if (kP + q < kmin || kP + q > kmax || kP + q < 1) continue;
-      int64_t len = (int64_t)binom(CB, q);
-      if (b0 + len > 0 && b0 < g_end - g_begin) any = true;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------ producer ----
+    if (lane != 0) return;
+    const uint64_t pol_near = l2_policy(false), pol_far = l2_policy(true);
+    uint32_t pJ = 0;
+    for (uint32_t seq = 0;; ++seq) {
+      unsigned P = kEndBlock;
+      for (;;) {
+        const unsigned c = atomicAdd(counter, 1u);
+        if (c >= blk_end - blk_begin) break;
+        if (!active || active[blk_begin + c]) {
+          P = blk_begin + c;
+          break;
+        }
+      }
+      unsigned prem = P == kEndBlock ? 0u : P;
+      for (bool first = true;; first = false) {
+        const int slot = pJ % kRing;
+        if (pJ >= kRing) mbar_wait(&sm.empty[slot], ((pJ / kRing) - 1) & 1u);
+        if (first) blkq[seq % kBlkQ] = P;          // published by the arrive below
+        if (P == kEndBlock) {
+          mbar_arrive(&sm.full[slot]);             // tx-free arrival: the end marker
+          return;
+        }
+        unsigned src = P;
+        uint64_t pol = pol_near;
+        if (prem) {
+          const int j = 31 - __clz(prem);
+          prem &= ~(1u << j);
+          src = P ^ (1u << j);
+          if (j >= near_bits) pol = pol_far;
+        }
+        mbar_expect_tx(&sm.full[slot], kBlkBytes);
+        tma_load_1d(sm.ring[slot], table + (int64_t)src * BLK, kBlkBytes, &sm.full[slot], pol);
+        ++pJ;
+        if (src == P) break;                       // own block issued: block complete
+      }
     }
-    if (!any) return;
   }
-  const int cnt = s_cnt;
-  if (tid == 32) {
-    const uint64_t pol_own = l2_policy(false);
-    mbar_expect_tx(&bars[kStages], kBlkBytes);
-    tma_load_1d(own, table + P * BLK, kBlkBytes, &bars[kStages], pol_own);
-    for (int i = 0; i < cnt && i < kStages; ++i) {
-      const unsigned nb = s_nb[i];
-      const bool far = ((P ^ (int64_t)nb) >> near_bits) != 0;
-      mbar_expect_tx(&bars[i], kBlkBytes);
-      tma_load_1d(ring[i], table + (int64_t)nb * BLK, kBlkBytes, &bars[i], l2_policy(far));
-    }
-  }
-  double acc[PER];
-#pragma unroll
-  for (int r = 0; r < PER; ++r) acc[r] = 0.0;
-  for (int i = 0; i < cnt; ++i) {
-    const int st = i % kStages;
-    mbar_wait(&bars[st], (uint32_t)((i / kStages) & 1));
-#pragma unroll
-    for (int r = 0; r < PER; ++r) acc[r] += ring[st][swz(tid + 256 * r)];
-    __syncthreads();                             // stage consumed by every thread
-    if (tid == 32 && i + kStages < cnt) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const unsigned nb = s_nb[i + kStages];
-      const bool far = ((P ^ (int64_t)nb) >> near_bits) != 0;
-      mbar_expect_tx(&bars[st], kBlkBytes);
-      tma_load_1d(ring[st], table + (int64_t)nb * BLK, kBlkBytes, &bars[st], l2_policy(far));
-    }
-  }
-  mbar_wait(&bars[kStages], 0);
-#pragma unroll
-  for (int r = 0; r < PER; ++r) {
-    const int e = tid + 256 * r;
-    double s = acc[r];
-#pragma unroll
-    for (int t = 0; t < CB; ++t)
-      if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
-    nbs[swz(e)] = s;
-  }
-  __syncthreads();
+
+  // -------------------------------------------------------- consumers ----
   const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
   const double e1 = et ? et[1] : 0.0;
-  for (int q = 0; q <= CB; ++q) {
-    const int k = kP + q;
-    if (k < kmin || k > kmax || k < 1) continue;
-    const int64_t b0 = s_base[q];
-    const int len = (int)binom(CB, q);
-    const int start = c_runstart[q];
-    const double kd = (double)k;
-    double ek = 0.0, ek1 = 0.0;
-    if (et) {
-      ek = et[k];
-      ek1 = et[k - 1];
+  const int64_t rows = g_end - g_begin;
+  int sw[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) sw[r] = swz(tid + kStencilThreads * r);
+  uint32_t J = 0;
+  for (uint32_t seq = 0;; ++seq) {
+    const int buf = seq & 1;
+    mbar_wait(&sm.full[J % kRing], (J / kRing) & 1u);   // first job of the block (or the end)
+    const unsigned P = *(volatile unsigned *)&blkq[seq % kBlkQ];
+    if (P == kEndBlock) break;
+    const int kP = __popc(P);
+    if (tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
+    double acc[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) acc[r] = 0.0;
+    for (int m = 0; m < kP; ++m, ++J) {
+      const int slot = J % kRing;
+      mbar_wait(&sm.full[slot], (J / kRing) & 1u);
+      const double *src = sm.ring[slot];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) acc[r] += src[sw[r]];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[slot]);
     }
-    for (int t = tid; t < len; t += 256) {
+    const int slot = J % kRing;
+    mbar_wait(&sm.full[slot], (J / kRing) & 1u);
+    const double *own = sm.ring[slot];
+    double *nbs = sm.nbs[buf];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int e = tid + kStencilThreads * r;
+      double s = acc[r];
+#pragma unroll
+      for (int t = 0; t < CB; ++t)
+        if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
+      nbs[sw[r]] = s;
+    }
+    named_bar_sync(1, kStencilThreads);           // nbs[buf] and base[buf] complete
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t w = sm.run[tid + kStencilThreads * r];
+      const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
+      const int64_t b0 = sm.base[buf][q];
+      if (b0 == kNoRun) continue;
+      const int k = kP + q;
       const int64_t row = b0 + t;
-      if (row < 0 || row >= g_end - g_begin) continue;
-      const int e = __ldg(g_runmask + start + t);
+      if (row < 0 || row >= rows) continue;
       const double l = own[swz(e)], nb = nbs[swz(e)];
+      const double kd = (double)k;
       double tc, dtc, o;
       if (et) {
+        const double ek = et[k], ek1 = et[k - 1];
         tc = -0.5 * l - kd * e1 + ek;
         dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
         o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
@@ -448,6 +533,9 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       __stcs(out + 2 * plane + oi, o);
       __stcs(out + 3 * plane + oi, tc + dtc);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);  // own slot free
+    ++J;
   }
 }
 
@@ -713,6 +801,14 @@ void upload_tables() {
   cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));
+  {
+    uint64_t st[CB + 1];
+    for (int q = 0; q <= CB; ++q) {
+      st[q] = 0;
+      for (int t = 0; t < q; ++t) st[q] += host_binom(CB - 1 - t, q - t);
+    }
+    cudaMemcpyToSymbol(c_suffix_term, st, sizeof(st));
+  }
   uploaded_for = dev;
 }
 
@@ -818,6 +914,48 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   return acc;
 }
 
+// Persistent stencil launch over table blocks [blk_begin, blk_end): one
+// CTA per resident slot (SMs x occupancy).  For a partial rank range the
+// blocks without output are flagged first (one thread per block) and
+// skipped without streaming them.
+static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
+                          int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
+                          unsigned blk_begin, unsigned blk_end, int near_bits, bool partial,
+                          bool flags_ready, cudaStream_t s) {
+  const unsigned nblocks = 1u << (N - CB);
+  uint8_t *active = partial ? reinterpret_cast<uint8_t *>(w.ready) : nullptr;
+  if (partial && !flags_ready) {
+    k_block_active<<<(nblocks + 255) / 256, 256, 0, s>>>(N, kmin, kmax, w.offs, g_begin, g_end,
+                                                          nblocks, active);
+    int st = check_launch("k_block_active");
+    if (st) return st;
+  }
+  static thread_local int smem_set_for = -1;
+  static thread_local int grid_cap = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int smem = (int)sizeof(StencilSmem);
+  if (smem_set_for != dev) {
+    cudaFuncSetAttribute(k_lattice_measures, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures, kStencilThreads + 32,
+                                                  smem);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    smem_set_for = dev;
+  }
+  const unsigned n = blk_end - blk_begin;
+  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
+  if (grid == 0) return HOI_OK;
+  const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+  k_lattice_measures<<<grid, kStencilThreads + 32, smem, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
+                                                          w.offs, g_begin, g_end, out, plane,
+                                                          blk_begin, blk_end, active, near_bits,
+                                                          w.counter);
+  return check_launch("k_lattice_measures");
+}
+
 int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
                      int kmax, int64_t g_begin, int64_t g_end, double *out, cudaStream_t s) {
   upload_binomials();
@@ -826,12 +964,9 @@ int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstri
   int64_t h_off[MAXV + 1];
   const int64_t total = total_rows(N, kmin, kmax, h_off);
   cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
-  const int64_t plane = (g_end - g_begin) * (int64_t)D;
-  const int partial = (g_begin > 0 || g_end < total) ? 1 : 0;
-  k_lattice_measures<<<1u << (N - CB), 256, 0, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
-                                                    w.offs, g_begin, g_end, out, plane, 0,
-                                                    default_near_bits(N - CB), partial);
-  return check_launch("k_lattice_measures");
+  const bool partial = g_begin > 0 || g_end < total;
+  return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, 0u,
+                        1u << (N - CB), default_near_bits(N - CB), partial, false, s);
 }
 
 // Two-stream pipeline over chunks of 2^w table blocks: the table of chunk
@@ -880,8 +1015,7 @@ int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta,
   PipeRes &pr = pipe_res(nchunks + 1);
   cudaEventRecord(pr.ev[nchunks], s);
   cudaStreamWaitEvent(pr.aux, pr.ev[nchunks], 0);
-  const int64_t plane = (g_end - g_begin) * (int64_t)D;
-  const int partial = (g_begin > 0 || g_end < total) ? 1 : 0;
+  const bool partial = g_begin > 0 || g_end < total;
   const int near_bits = wb + 1 < nP ? wb + 1 : nP;   // neighbours in this or the previous chunk
   const unsigned ctas = 1u << (wb - b);
   for (int c = 0; c < nchunks; ++c) {
@@ -889,10 +1023,9 @@ int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta,
     if ((st = check_launch("k_lattice_table"))) return st;
     cudaEventRecord(pr.ev[c], pr.aux);
     cudaStreamWaitEvent(s, pr.ev[c], 0);
-    k_lattice_measures<<<1u << wb, 256, 0, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
-                                                w.offs, g_begin, g_end, out, plane,
-                                                (int64_t)c << wb, near_bits, partial);
-    if ((st = check_launch("k_lattice_measures"))) return st;
+    st = launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, (unsigned)c << wb,
+                        (unsigned)(c + 1) << wb, near_bits, partial, c > 0, s);
+    if (st) return st;
   }
   return HOI_OK;
 }
