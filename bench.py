@@ -45,6 +45,7 @@ def args_():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-percell", action="store_true", help="skip the per-n-plet engine leg")
     return p.parse_args()
 
 
@@ -376,7 +377,7 @@ def b200_arm(a):
     del out
     torch.cuda.empty_cache()
     fp64 = None
-    if rank == 0:
+    if rank == 0 and (engine_used == 1 or not a.no_percell):
         fp64 = percell_roofline(torch, lib, nat, covs, g0, g1, ms if engine_used == 1 else None)
         if engine_used == 1:
             roof = fp64

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace hoib {
@@ -123,7 +124,7 @@ struct Leaf {
     // include: pivot a00, Schur complement of the rest
     const double p = a[0];
     bad |= !(p > kMinPivot);
-    const double rp = 1.0 / p;
+    const double rp = __drcp_rn(p);
     double in[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
 #pragma unroll
     for (int i = 1; i < R; ++i) {
@@ -146,17 +147,36 @@ struct Leaf<0, SW> {
   }
 };
 
-// Phase 1: one CTA per pattern of the "fixed" prefix variables b..N-CB-1;
-// its 8 warps expand the 2^b patterns of prefix variables 0..b-1, and each
-// lane of a warp owns one pattern of F0..F4 and recurses over F5..F9.
+// One Schur step on a symmetric matrix kept as its lower triangle (row
+// stride ld): eliminate pivot j, A[i][l] -= A[i][j] A[l][j] / A[j][j] for
+// j < l <= i < n.  Thread t of `nt` (nt a multiple of 32) owns column
+// j+1 + (t & 31) and every (nt/32)-th row below the diagonal -- no integer
+// division, only the triangle that later steps read.
+__device__ __forceinline__ void schur_lower(double *A, int ld, int n, int j, int t, int nt) {
+  const double rp = __drcp_rn(A[j * ld + j]);
+  const int l = j + 1 + (t & 31);
+  if (l < n) {
+    const double alj = A[l * ld + j] * rp;
+    for (int i = l + (t >> 5); i < n; i += nt >> 5) A[i * ld + l] = fma(-A[i * ld + j], alj, A[i * ld + l]);
+  }
+}
+
+// Phase 1: one CTA per pattern of the "fixed" prefix variables b..N-CB-1
+// (b = 6).  The CTA eliminates its fixed variables once; warp w eliminates
+// the set bits of w among prefix variables 0..2 once (shared by its 8
+// patterns), then each of its 8 patterns of variables 3..5 from that state
+// -- every warp runs the same mix of patterns, so the CTA tail is short.
+// Each lane of a warp owns one pattern of F0..F4 and recurses over F5..F9
+// in registers.
 __global__ void __launch_bounds__(256, 2)
 k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
                 double *__restrict__ table, int *__restrict__ flag, unsigned cta_off) {
   const unsigned cta = blockIdx.x + cta_off;
   __shared__ double2 s_logtab[256];
   constexpr int MS = MAXV + 1;
+  constexpr int WS = MAXB + CB;                    // per-warp matrix stride
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
-  __shared__ double W[8][(MAXB + CB) * (MAXB + CB)];  // per-warp (b+CB)^2 work
+  __shared__ double W[8][2][WS * WS];              // per-warp base / work (lower triangles)
   __shared__ int vars[MAXV];
   __shared__ int s_nfix;
   __shared__ double s_m0;
@@ -176,12 +196,10 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   }
   __syncthreads();
   const int nfix = s_nfix, m = nfix + b + CB;
-  for (int x = tid; x < m * m; x += blockDim.x) {
-    int i = x / m, l = x - i * m;
-    M[i * MS + l] = corr[((int64_t)vars[i] * N + vars[l]) * D + d];
-  }
+  for (int i = tid >> 5; i < m; i += 8)
+    if (lane <= i) M[i * MS + lane] = corr[((int64_t)vars[i] * N + vars[lane]) * D + d];
   __syncthreads();
-  // eliminate the fixed prefix variables (right-looking, full square)
+  // eliminate the fixed prefix variables (right-looking, lower triangle)
   double m0 = 1.0;
   int e0 = 0;
   for (int j = 0; j < nfix; ++j) {
@@ -190,12 +208,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(m0, e0, p);
     }
-    const double rp = 1.0 / p;
-    const int r = m - j - 1;
-    for (int x = tid; x < r * r; x += blockDim.x) {
-      int i = j + 1 + x / r, l = j + 1 + x % r;
-      M[i * MS + l] = fma(-M[i * MS + j] * rp, M[j * MS + l], M[i * MS + l]);
-    }
+    schur_lower(M, MS, m, j, tid, 256);
     __syncthreads();
   }
   if (tid == 0) {
@@ -204,24 +217,46 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   }
   __syncthreads();
   const int w = b + CB;                            // expansion size
-  double *Wm = W[warp];
+  const int blo = b < 3 ? b : 3;                   // prefix bits fixed per warp
   const double *S0 = M + nfix * MS + nfix;
-  for (int u = warp; u < (1 << b); u += 8) {
-    for (int x = lane; x < w * w; x += 32) Wm[x] = S0[(x / w) * MS + (x % w)];
+  double *Wb = W[warp][0], *Wm = W[warp][1];
+  __shared__ double s_mb[8];
+  __shared__ int s_eb[8];
+  const int ulo = warp & ((1 << blo) - 1);
+  if (warp < (1 << blo)) {
+    double mb = s_m0;
+    int ebase = s_e0;
+    for (int i = 0; i < w; ++i)
+      if (lane <= i) Wb[i * WS + lane] = S0[i * MS + lane];
     __syncwarp();
-    double mu = s_m0;
-    int eu = s_e0;
-    for (int j = 0; j < b; ++j) {
+    for (int j = 0; j < blo; ++j) {
+      if (!((ulo >> j) & 1)) continue;             // warp-uniform
+      const double p = Wb[j * WS + j];
+      if (!(p > kMinPivot)) s_bad = 1;
+      lp_mul(mb, ebase, p);
+      schur_lower(Wb, WS, w, j, lane, 32);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      s_mb[warp] = mb;
+      s_eb[warp] = ebase;
+    }
+    __syncwarp();
+  }
+  for (int uh = 0; uh < (1 << (b - blo)); ++uh) {
+    if (warp >= (1 << blo)) break;
+    const int u = ulo | (uh << blo);
+    for (int i = 0; i < w; ++i)
+      if (lane <= i) Wm[i * WS + lane] = Wb[i * WS + lane];
+    __syncwarp();
+    double mu = s_mb[warp];
+    int eu = s_eb[warp];
+    for (int j = blo; j < b; ++j) {
       if (!((u >> j) & 1)) continue;               // warp-uniform
-      const double p = Wm[j * w + j];
-      if (!(p > kMinPivot) && lane == 0) s_bad = 1;
+      const double p = Wm[j * WS + j];
+      if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(mu, eu, p);
-      const double rp = 1.0 / p;
-      const int r = w - j - 1;
-      for (int x = lane; x < r * r; x += 32) {
-        int i = j + 1 + x / r, l = j + 1 + x % r;
-        Wm[i * w + l] = fma(-Wm[i * w + j] * rp, Wm[j * w + l], Wm[i * w + l]);
-      }
+      schur_lower(Wm, WS, w, j, lane, 32);
       __syncwarp();
     }
     // suffix Schur complement C = Wm[b.., b..] (CB x CB); each lane takes
@@ -230,7 +265,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
 #pragma unroll
     for (int i = 0; i < CB; ++i)
 #pragma unroll
-      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = Wm[(b + i) * w + (b + l)];
+      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = Wm[(b + i) * WS + (b + l)];
     __syncwarp();
     double ml = mu;
     int el = eu;
@@ -240,7 +275,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       const bool inc = (lane >> j) & 1;
       const double p = c[j * (j + 1) / 2 + j];
       if (inc && !(p > kMinPivot)) bad = 1;
-      const double f = inc ? 1.0 / p : 0.0;
+      const double f = inc ? __drcp_rn(p) : 0.0;
       if (inc) lp_mul(ml, el, p);
 #pragma unroll
       for (int i = j + 1; i < CB; ++i) {
@@ -294,6 +329,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
   }
 }
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
   uint64_t p;
   if (evict_first)
@@ -311,12 +351,13 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
-constexpr int kRing = 6;            // 8 KB table blocks in flight per CTA
 constexpr int kConsumerWarps = 8;
 constexpr int kStencilThreads = 32 * kConsumerWarps;   // consumers; + 1 producer warp
 constexpr int PER = BLK / kStencilThreads;
 
-// Dynamic shared memory of the stencil kernel.
+// Dynamic shared memory of the stencil kernel (kRing 8 KB table blocks in
+// flight per CTA).
+template <int kRing>
 struct StencilSmem {
   double ring[kRing][BLK];           // TMA destination ring (48 KB)
   double nbs[2][BLK];                // sum of the k leave-one-out log-dets per entry
@@ -397,14 +438,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 // after the only per-block barrier (named, consumers only; nbs/base are
 // double-buffered) -- writes the four measures of each run (P, q) as one
 // coalesced, contiguous span of the order-major lexicographic output.
-__global__ void __launch_bounds__(kStencilThreads + 32, 3)
+template <int kRing, int kMinCtas>
+__global__ void __launch_bounds__(kStencilThreads + 32, kMinCtas)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
                    unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
-                   int near_bits, unsigned *__restrict__ counter) {
+                   int near_bits, unsigned *__restrict__ counter, int own_last) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  StencilSmem &sm = *reinterpret_cast<StencilSmem *>(smem_raw);
+  StencilSmem<kRing> &sm = *reinterpret_cast<StencilSmem<kRing> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -426,6 +468,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     // ------------------------------------------------------ producer ----
     if (lane != 0) return;
     const uint64_t pol_near = l2_policy(false), pol_far = l2_policy(true);
+    const uint64_t pol_own = own_last ? l2_policy_last() : pol_near;
     uint32_t pJ = 0;
     for (uint32_t seq = 0;; ++seq) {
       unsigned P = kEndBlock;
@@ -447,12 +490,12 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
           return;
         }
         unsigned src = P;
-        uint64_t pol = pol_near;
+        uint64_t pol = pol_own;
         if (prem) {
           const int j = 31 - __clz(prem);
           prem &= ~(1u << j);
           src = P ^ (1u << j);
-          if (j >= near_bits) pol = pol_far;
+          pol = j >= near_bits ? pol_far : pol_near;
         }
         mbar_expect_tx(&sm.full[slot], kBlkBytes);
         tma_load_1d(sm.ring[slot], table + (int64_t)src * BLK, kBlkBytes, &sm.full[slot], pol);
@@ -466,9 +509,19 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
   const double e1 = et ? et[1] : 0.0;
   const int64_t rows = g_end - g_begin;
-  int sw[PER];
+  // Each thread owns PAIRS entry pairs (e, e+1), e = 2*pi, pi = tid + 256 r.
+  // swz(e+1) == swz(e) ^ 1, so a pair is one aligned 16-byte word whose
+  // halves are swapped when bit 5 of e is set (flip): every neighbour block
+  // is consumed with 128-bit loads and summed in memory order.
+  constexpr int PAIRS = PER / 2;
+  int pw[PAIRS];
+  bool flip[PAIRS];
 #pragma unroll
-  for (int r = 0; r < PER; ++r) sw[r] = swz(tid + kStencilThreads * r);
+  for (int r = 0; r < PAIRS; ++r) {
+    const int e = 2 * (tid + kStencilThreads * r);
+    pw[r] = swz(e) & ~1;
+    flip[r] = (e >> 5) & 1;
+  }
   uint32_t J = 0;
   for (uint32_t seq = 0;; ++seq) {
     const int buf = seq & 1;
@@ -477,15 +530,19 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     if (P == kEndBlock) break;
     const int kP = __popc(P);
     if (tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
-    double acc[PER];
+    double2 acc[PAIRS];
 #pragma unroll
-    for (int r = 0; r < PER; ++r) acc[r] = 0.0;
+    for (int r = 0; r < PAIRS; ++r) acc[r] = make_double2(0.0, 0.0);
     for (int m = 0; m < kP; ++m, ++J) {
       const int slot = J % kRing;
       mbar_wait(&sm.full[slot], (J / kRing) & 1u);
       const double *src = sm.ring[slot];
 #pragma unroll
-      for (int r = 0; r < PER; ++r) acc[r] += src[sw[r]];
+      for (int r = 0; r < PAIRS; ++r) {
+        const double2 v = *reinterpret_cast<const double2 *>(src + pw[r]);
+        acc[r].x += v.x;
+        acc[r].y += v.y;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
     }
@@ -494,13 +551,23 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const double *own = sm.ring[slot];
     double *nbs = sm.nbs[buf];
 #pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const int e = tid + kStencilThreads * r;
-      double s = acc[r];
+    for (int r = 0; r < PAIRS; ++r) {
+      const int e0 = 2 * (tid + kStencilThreads * r);
+      const double2 ov = *reinterpret_cast<const double2 *>(own + pw[r]);
+      const double o0 = flip[r] ? ov.y : ov.x;
+      double s0 = flip[r] ? acc[r].y : acc[r].x;
+      double s1 = (flip[r] ? acc[r].x : acc[r].y) + o0;   // bit-0 neighbour of e0+1 is e0
 #pragma unroll
-      for (int t = 0; t < CB; ++t)
-        if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
-      nbs[sw[r]] = s;
+      for (int t = 1; t < CB; ++t) {
+        if ((e0 >> t) & 1) {
+          const int n0 = e0 ^ (1 << t);
+          const double2 v = *reinterpret_cast<const double2 *>(own + (swz(n0) & ~1));
+          const bool f = (n0 >> 5) & 1;
+          s0 += f ? v.y : v.x;
+          s1 += f ? v.x : v.y;
+        }
+      }
+      *reinterpret_cast<double2 *>(nbs + pw[r]) = flip[r] ? make_double2(s1, s0) : make_double2(s0, s1);
     }
     named_bar_sync(1, kStencilThreads);           // nbs[buf] and base[buf] complete
 #pragma unroll
@@ -903,7 +970,10 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   return check_launch("k_lattice_table");
 }
 
-static int default_near_bits(int nP) { return nP > kFarBits + kMinNearBits ? nP - kFarBits : nP; }
+// Neighbour reads beyond this bit use evict-first loads.  Measured on B200
+// (cfg4, persistent stencil): marking any neighbour evict-first costs time
+// (17.1 ms with none vs 17.8 ms with the top 6 bits), so none is marked.
+static int default_near_bits(int nP) { return nP; }
 
 static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   int64_t acc = 0;
@@ -912,6 +982,34 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
     acc += (int64_t)host_binom(N, k);
   }
   return acc;
+}
+
+template <int R, int C>
+static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
+                       int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
+                       int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
+                       int near_bits, int own_last, cudaStream_t s) {
+  static thread_local int set_for = -1;
+  static thread_local int grid_cap = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int smem = (int)sizeof(StencilSmem<R>);
+  if (set_for != dev) {
+    cudaFuncSetAttribute(k_lattice_measures<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C>,
+                                                  kStencilThreads + 32, smem);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    set_for = dev;
+  }
+  const unsigned n = blk_end - blk_begin;
+  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
+  if (grid == 0) return HOI_OK;
+  k_lattice_measures<R, C><<<grid, kStencilThreads + 32, smem, s>>>(
+      w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
+      blk_end, active, near_bits, w.counter, own_last);
+  return check_launch("k_lattice_measures");
 }
 
 // Persistent stencil launch over table blocks [blk_begin, blk_end): one
@@ -930,31 +1028,24 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     int st = check_launch("k_block_active");
     if (st) return st;
   }
-  static thread_local int smem_set_for = -1;
-  static thread_local int grid_cap = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int smem = (int)sizeof(StencilSmem);
-  if (smem_set_for != dev) {
-    cudaFuncSetAttribute(k_lattice_measures, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures, kStencilThreads + 32,
-                                                  smem);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
-    smem_set_for = dev;
-  }
-  const unsigned n = blk_end - blk_begin;
-  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
-  if (grid == 0) return HOI_OK;
+  // experiment knobs (defaults are the measured best)
+  // measured on B200 (cfg4): 4 CTAs x 4-slot rings beat 3 x 6 and 2 x 10
+  // (more independent in-order streams per SM), own block evict_last
+  static const int ring = getenv("HOI_RING") ? atoi(getenv("HOI_RING")) : 4;
+  static const int own_last = getenv("HOI_OWN_LAST") ? atoi(getenv("HOI_OWN_LAST")) : 1;
+  if (getenv("HOI_NEAR_BITS")) near_bits = atoi(getenv("HOI_NEAR_BITS"));
   const int64_t plane = (g_end - g_begin) * (int64_t)D;
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
-  k_lattice_measures<<<grid, kStencilThreads + 32, smem, s>>>(w.table, N, D, d, kmin, kmax, eta, kstride,
-                                                          w.offs, g_begin, g_end, out, plane,
-                                                          blk_begin, blk_end, active, near_bits,
-                                                          w.counter);
-  return check_launch("k_lattice_measures");
+  if (ring == 10)
+    return run_stencil<10, 2>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
+                              blk_begin, blk_end, active, near_bits, own_last, s);
+  if (ring == 4)
+    return run_stencil<4, 4>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
+                             blk_begin, blk_end, active, near_bits, own_last, s);
+  return run_stencil<6, 3>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
+                           blk_begin, blk_end, active, near_bits, own_last, s);
 }
+
 
 int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
                      int kmax, int64_t g_begin, int64_t g_end, double *out, cudaStream_t s) {
