@@ -30,6 +30,9 @@ void fill_binomials(uint64_t *h);   // host table, kBinomN^2 entries
 // Without relocatable device code every translation unit owns its own copy
 // of the constant table, so the uploader is instantiated per unit too.
 static __constant__ uint64_t c_binom[kBinomN * kBinomN];
+// Global copy for lookups whose indices differ across a warp (constant
+// memory serialises divergent addresses; this one goes through L1).
+static __device__ uint64_t g_binom_l1[kBinomN * kBinomN];
 static inline void upload_binomials() {
   static thread_local int uploaded_for = -1;
   int dev = 0;
@@ -38,11 +41,15 @@ static inline void upload_binomials() {
   uint64_t h[kBinomN * kBinomN];
   fill_binomials(h);
   cudaMemcpyToSymbol(c_binom, h, sizeof(h));
+  cudaMemcpyToSymbol(g_binom_l1, h, sizeof(h));
   uploaded_for = dev;
 }
 
 __device__ __forceinline__ uint64_t binom(int n, int m) {
   return (m < 0 || n < 0 || m > n) ? 0ull : c_binom[n * kBinomN + m];
+}
+__device__ __forceinline__ uint64_t binom_l1(int n, int m) {
+  return (m < 0 || n < 0 || m > n) ? 0ull : __ldg(g_binom_l1 + n * kBinomN + m);
 }
 
 // ------------------------------------------------- floating-point helpers --

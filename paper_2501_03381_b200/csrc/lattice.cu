@@ -168,15 +168,17 @@ __device__ __forceinline__ void schur_lower(double *A, int ld, int n, int j, int
 // -- every warp runs the same mix of patterns, so the CTA tail is short.
 // Each lane of a warp owns one pattern of F0..F4 and recurses over F5..F9
 // in registers.
-__global__ void __launch_bounds__(256, 2)
+template <int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW)
 k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
                 double *__restrict__ table, int *__restrict__ flag, unsigned cta_off) {
+  constexpr int NT = 32 * NW;
   const unsigned cta = blockIdx.x + cta_off;
   __shared__ double2 s_logtab[256];
   constexpr int MS = MAXV + 1;
   constexpr int WS = MAXB + CB;                    // per-warp matrix stride
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
-  __shared__ double W[8][2][WS * WS];              // per-warp base / work (lower triangles)
+  __shared__ double W[NW][2][WS * WS];             // per-warp base / work (lower triangles)
   __shared__ int vars[MAXV];
   __shared__ int s_nfix;
   __shared__ double s_m0;
@@ -184,7 +186,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nP = N - CB;
-  s_logtab[tid] = c_logtab[tid];
+  for (int x = tid; x < 256; x += NT) s_logtab[x] = c_logtab[x];
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
@@ -196,7 +198,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   }
   __syncthreads();
   const int nfix = s_nfix, m = nfix + b + CB;
-  for (int i = tid >> 5; i < m; i += 8)
+  for (int i = tid >> 5; i < m; i += NW)
     if (lane <= i) M[i * MS + lane] = corr[((int64_t)vars[i] * N + vars[lane]) * D + d];
   __syncthreads();
   // eliminate the fixed prefix variables (right-looking, lower triangle)
@@ -208,7 +210,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(m0, e0, p);
     }
-    schur_lower(M, MS, m, j, tid, 256);
+    schur_lower(M, MS, m, j, tid, NT);
     __syncthreads();
   }
   if (tid == 0) {
@@ -217,11 +219,12 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   }
   __syncthreads();
   const int w = b + CB;                            // expansion size
-  const int blo = b < 3 ? b : 3;                   // prefix bits fixed per warp
+  constexpr int LW = NW == 8 ? 3 : NW == 4 ? 2 : NW == 2 ? 1 : 0;
+  const int blo = b < LW ? b : LW;                 // prefix bits fixed per warp
   const double *S0 = M + nfix * MS + nfix;
   double *Wb = W[warp][0], *Wm = W[warp][1];
-  __shared__ double s_mb[8];
-  __shared__ int s_eb[8];
+  __shared__ double s_mb[NW];
+  __shared__ int s_eb[NW];
   const int ulo = warp & ((1 << blo) - 1);
   if (warp < (1 << blo)) {
     double mb = s_m0;
@@ -966,7 +969,7 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
-  k_lattice_table<<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag, 0u);
+  k_lattice_table<8><<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag, 0u);
   return check_launch("k_lattice_table");
 }
 
@@ -988,9 +991,9 @@ template <int R, int C>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                        int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
-                       int near_bits, int own_last, cudaStream_t s) {
+                       int near_bits, int own_last, int per_sm_cap, cudaStream_t s) {
   static thread_local int set_for = -1;
-  static thread_local int grid_cap = 0;
+  static thread_local int grid_cap = 0, n_sms = 0, max_per_sm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   const int smem = (int)sizeof(StencilSmem<R>);
@@ -1000,11 +1003,15 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C>,
                                                   kStencilThreads + 32, smem);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    max_per_sm = per_sm > 0 ? per_sm : 1;
+    n_sms = sms;
+    grid_cap = sms * max_per_sm;
     set_for = dev;
   }
   const unsigned n = blk_end - blk_begin;
-  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
+  unsigned cap = (unsigned)grid_cap;
+  if (per_sm_cap > 0 && per_sm_cap < max_per_sm) cap = (unsigned)(n_sms * per_sm_cap);
+  const unsigned grid = n < cap ? n : cap;
   if (grid == 0) return HOI_OK;
   k_lattice_measures<R, C><<<grid, kStencilThreads + 32, smem, s>>>(
       w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
@@ -1019,7 +1026,7 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
 static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                           int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                           unsigned blk_begin, unsigned blk_end, int near_bits, bool partial,
-                          bool flags_ready, cudaStream_t s) {
+                          bool flags_ready, cudaStream_t s, int per_sm_cap = 0) {
   const unsigned nblocks = 1u << (N - CB);
   uint8_t *active = partial ? reinterpret_cast<uint8_t *>(w.ready) : nullptr;
   if (partial && !flags_ready) {
@@ -1038,12 +1045,12 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
   if (ring == 10)
     return run_stencil<10, 2>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                              blk_begin, blk_end, active, near_bits, own_last, s);
+                              blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
   if (ring == 4)
     return run_stencil<4, 4>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                             blk_begin, blk_end, active, near_bits, own_last, s);
+                             blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
   return run_stencil<6, 3>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                           blk_begin, blk_end, active, near_bits, own_last, s);
+                           blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
 }
 
 
@@ -1097,7 +1104,10 @@ int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta,
   LatticeWs w = ws_view(ws, N);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
-  const int wb = nP < 13 ? nP : 13;                 // chunk = 2^wb blocks (64 MB of table)
+  static const int wb_env = getenv("HOI_PIPE_WB") ? atoi(getenv("HOI_PIPE_WB")) : 16;
+  static const int tnw = getenv("HOI_TABLE_NW") ? atoi(getenv("HOI_TABLE_NW")) : 4;
+  static const int sper = getenv("HOI_STENCIL_PER_SM") ? atoi(getenv("HOI_STENCIL_PER_SM")) : 3;
+  const int wb = nP < wb_env ? nP : wb_env;         // chunk = 2^wb blocks
   const int nchunks = 1 << (nP - wb);
   int64_t h_off[MAXV + 1];
   const int64_t total = total_rows(N, kmin, kmax, h_off);
@@ -1107,15 +1117,18 @@ int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta,
   cudaEventRecord(pr.ev[nchunks], s);
   cudaStreamWaitEvent(pr.aux, pr.ev[nchunks], 0);
   const bool partial = g_begin > 0 || g_end < total;
-  const int near_bits = wb + 1 < nP ? wb + 1 : nP;   // neighbours in this or the previous chunk
+  const int near_bits = default_near_bits(nP);
   const unsigned ctas = 1u << (wb - b);
   for (int c = 0; c < nchunks; ++c) {
-    k_lattice_table<<<ctas, 256, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
+    if (tnw == 8)
+      k_lattice_table<8><<<ctas, 256, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
+    else
+      k_lattice_table<4><<<ctas, 128, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
     if ((st = check_launch("k_lattice_table"))) return st;
     cudaEventRecord(pr.ev[c], pr.aux);
     cudaStreamWaitEvent(s, pr.ev[c], 0);
     st = launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, (unsigned)c << wb,
-                        (unsigned)(c + 1) << wb, near_bits, partial, c > 0, s);
+                        (unsigned)(c + 1) << wb, near_bits, partial, c > 0, s, sper);
     if (st) return st;
   }
   return HOI_OK;
@@ -1138,7 +1151,16 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
   // Sequential table -> stencil measured faster on B200 (25.0 ms for cfg4)
   // than the chunked two-stream pipeline (26.1 ms); lattice_pipeline stays
   // available for the measurements in DESIGN.md.
+  static const int pipe = getenv("HOI_PIPE") ? atoi(getenv("HOI_PIPE")) : 0;
   for (int d = 0; d < D; ++d) {
+    if (pipe) {
+      int st = lattice_pipeline(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
+                                ws_bytes, s);
+      if (st) return st;
+      st = lattice_status(ws, N, s);
+      if (st) return st;
+      continue;
+    }
     int st = lattice_table(corr, N, D, d, ws, ws_bytes, s);
     if (st) return st;
     st = lattice_status(ws, N, s);      // not PD: the caller reruns with engine 1

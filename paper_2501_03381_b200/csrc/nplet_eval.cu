@@ -1,297 +1,15 @@
-// Engine 1: per-(n-plet, dataset) evaluation.
-//
-// One thread owns one (n-plet, dataset) unit.  For K <= kMaxRegK the K x K
-// packed lower triangle lives in registers (K is a template parameter and
-// every loop is fully unrolled, so all indices are compile-time); larger K
-// use the same code with a runtime K (local memory).
-//
-// Per unit:  gather R_S from the L2-resident correlation matrix (dataset
-// index fastest, so the D units of one n-plet read one cache line) ->
-// square-root-free LDL^T (log det = sum log d_j) -> in-place inverse of the
-// unit lower factor U = L^-1 -> inverse diagonal (R_S^-1)_jj =
-// sum_i U_ij^2 / d_i (every leave-one-out determinant is
-// det(R_S) * (R_S^-1)_jj, ref:nplet_engine.py:267-273) -> fused epilogue
-// writing only tc, dtc, o, s (ref:measures.py:41-81).
-//
-// In the correlation form the per-variable log Sigma_jj terms cancel from
-// every measure, so with l = log det R_S and lam = sum_j log (R_S^-1)_jj:
-//   tc  = -l/2                 - k*eta1 + eta_k
-//   dtc = (l + lam)/2          + (k-1)*eta_k - k*eta_{k-1}
-//   o   = -l - lam/2           - k*eta1 - (k-2)*eta_k + k*eta_{k-1}
-//   s   = tc + dtc
-// (eta = finite-sample bias, ref:nplet_engine.py:295-321).
-//
-// Failure handling mirrors ref:nplet_engine.py:237-264: a non-positive (or
-// NaN) pivot triggers one retry of that matrix with Sigma_S + eps*I,
-// eps = 1e-10 * trace(Sigma_S) / k; a second failure records (row, dataset).
-#include "common.cuh"
+// Engine 1 host side: dispatch, unranking, mask compaction and the C ABI.
+// The per-unit kernels live in eval_kernels.cuh (see there).
+#include "eval_kernels.cuh"
 
 namespace hoib {
 
-constexpr int kMaxRegK = 12;
-
-struct EvalArgs {
-  const double *src;       // corr (N,N,D)  or matrix stack (M,K,K) when mats
-  const double *sdiag;     // (D,N) covariance diagonal or nullptr
-  const double *eta;       // (D,kstride) or nullptr
-  int kstride;
-  int N, D;
-  int mats;                // 1: raw matrix stack mode
-  const int32_t *idx;      // (B, idx_stride) or nullptr -> unrank
-  int64_t idx_stride;
-  const int64_t *row_map;  // output row of input row b, or nullptr
-  int64_t B;
-  uint64_t r0;             // unrank: local lexicographic rank of row 0
-  double *out;             // 4 planes, plane stride `plane`
-  int64_t plane;
-  int64_t out_row0;
-  double *logdet;          // (rows, D) or nullptr
-  double *invdiag;         // (rows, D, K) or scattered (rows, D, inv_n)
-  int inv_n;               // 0: dense K layout, >0: scatter by variable id
-  int32_t *err_count;
-  int64_t *err_coords;
-  int err_cap;
-};
-
-#define TRI(i, j) ((i) * ((i) + 1) / 2 + (j))
-
-__device__ __forceinline__ void unrank_lex(uint64_t r, int K, int N, int *s) {
-  int c = 0;
-  for (int p = 0; p < K; ++p) {
-    while (c < N) {
-      uint64_t b = binom(N - 1 - c, K - 1 - p);
-      if (b <= r) {
-        r -= b;
-        ++c;
-      } else {
-        break;
-      }
-    }
-    s[p] = c++;
-  }
-}
-
-template <int KT, bool FIXED>
-__device__ __forceinline__ void load_matrix(const EvalArgs &A, int64_t b, int d, int K,
-                                            const int (&s)[KT], double (&a)[KT * (KT + 1) / 2],
-                                            bool jitter) {
-  if (A.mats) {
-    const double *m = A.src + (int64_t)b * K * K;
-    double tr = 0.0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-#pragma unroll
-      for (int j = 0; j <= i; ++j) a[TRI(i, j)] = m[i * K + j];
-      tr += m[i * K + i];
-    }
-    if (jitter) {
-      double eps = 1e-10 * tr / (double)K;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        a[TRI(i, i)] += eps;
-      }
-    }
-    return;
-  }
-  const int N = A.N, D = A.D;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const double *row = A.src + ((int64_t)s[i] * N) * D + d;
-#pragma unroll
-    for (int j = 0; j <= i; ++j) a[TRI(i, j)] = __ldg(row + (int64_t)s[j] * D);
-  }
-  if (jitter) {
-    double tr = 0.0;
-    if (A.sdiag) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        tr += A.sdiag[(int64_t)d * N + s[i]];
-      }
-    } else {
-      tr = (double)K;
-    }
-    double eps = 1e-10 * tr / (double)K;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double sc = A.sdiag ? A.sdiag[(int64_t)d * N + s[i]] : 1.0;
-      a[TRI(i, i)] += eps / sc;
-    }
-  }
-}
-
-// LDL^T + unit-triangular inverse + inverse diagonal.  Returns false on a
-// non-positive / NaN pivot.  cs[j] = (M^-1)_jj; l = log det M; lam = sum log cs.
-template <int KT, bool FIXED>
-__device__ __forceinline__ bool ldl_invdiag(double (&a)[KT * (KT + 1) / 2], int K,
-                                            double (&cs)[KT], double &l, double &lam) {
-  double dinv[KT];
-  double col[KT];
-  LogProd pd;
-  pd.init();
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    double dj = a[TRI(j, j)];
-    if (!(dj > 0.0)) return false;
-    pd.mul(dj);
-    if ((j & 7) == 7) pd.renorm();
-    double r = 1.0 / dj;
-    dinv[j] = r;
-#pragma unroll
-    for (int i = j + 1; i < K; ++i) {
-      col[i] = a[TRI(i, j)];
-      a[TRI(i, j)] = col[i] * r;
-    }
-#pragma unroll
-    for (int i = j + 1; i < K; ++i) {
-      double lij = a[TRI(i, j)];
-#pragma unroll
-      for (int m = j + 1; m <= i; ++m) a[TRI(i, m)] = fma(-lij, col[m], a[TRI(i, m)]);
-    }
-  }
-  pd.renorm();
-  // U = L^-1 (unit lower), column by column, in place.
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-#pragma unroll
-    for (int i = j + 1; i < K; ++i) {
-      double acc = a[TRI(i, j)];
-#pragma unroll
-      for (int m = j + 1; m < i; ++m) acc = fma(a[TRI(i, m)], a[TRI(m, j)], acc);
-      a[TRI(i, j)] = -acc;
-    }
-  }
-  LogProd pl;
-  pl.init();
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    double sacc = dinv[j];
-#pragma unroll
-    for (int i = j + 1; i < K; ++i) {
-      double u = a[TRI(i, j)];
-      sacc = fma(u * u, dinv[i], sacc);
-    }
-    cs[j] = sacc;
-    pl.mul(sacc);
-    if ((j & 7) == 7) pl.renorm();
-  }
-  pl.renorm();
-  l = pd.log_value();
-  lam = pl.log_value();
-  return true;
-}
-
-template <int KT, bool FIXED>
-__device__ __forceinline__ void eval_unit(const EvalArgs &A, int64_t b, int d, int kdyn) {
-  const int K = FIXED ? KT : kdyn;
-  int s[KT];
-  if (!A.mats) {
-    if (A.idx) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        s[i] = A.idx[b * A.idx_stride + i];
-      }
-    } else {
-      unrank_lex(A.r0 + (uint64_t)b, K, A.N, s);
-    }
-  }
-  double a[KT * (KT + 1) / 2];
-  double cs[KT];
-  double l = 0.0, lam = 0.0;
-  load_matrix<KT, FIXED>(A, b, d, K, s, a, false);
-  bool ok = ldl_invdiag<KT, FIXED>(a, K, cs, l, lam);
-  if (!ok) {
-    load_matrix<KT, FIXED>(A, b, d, K, s, a, true);
-    ok = ldl_invdiag<KT, FIXED>(a, K, cs, l, lam);
-  }
-  const int64_t ob = A.row_map ? A.row_map[b] : A.out_row0 + b;
-  const int64_t o = ob * A.D + d;
-  if (!ok) {
-    int slot = atomicAdd(A.err_count, 1);
-    if (slot < A.err_cap) {
-      A.err_coords[2 * slot] = ob;
-      A.err_coords[2 * slot + 1] = d;
-    }
-    const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    if (A.out) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) A.out[q * A.plane + o] = nan;
-    }
-    if (A.logdet) A.logdet[o] = nan;
-    return;
-  }
-  if (A.out) {
-    double tc, dtc, oi;
-    const double kd = (double)K;
-    if (A.eta) {
-      const double *e = A.eta + (int64_t)d * A.kstride;
-      const double e1 = e[1], ek = e[K], ek1 = e[K - 1];
-      tc = -0.5 * l - kd * e1 + ek;
-      dtc = 0.5 * (l + lam) + (kd - 1.0) * ek - kd * ek1;
-      oi = -l - 0.5 * lam - kd * e1 - (kd - 2.0) * ek + kd * ek1;
-    } else {
-      tc = -0.5 * l;
-      dtc = 0.5 * (l + lam);
-      oi = -l - 0.5 * lam;
-    }
-    A.out[o] = tc;
-    A.out[A.plane + o] = dtc;
-    A.out[2 * A.plane + o] = oi;
-    A.out[3 * A.plane + o] = tc + dtc;
-  }
-  if (A.logdet || A.invdiag) {
-    // Sigma-space values (entropy_terms compat): log det Sigma_S =
-    // l + sum log sigma_j, (Sigma_S^-1)_jj = (R_S^-1)_jj / sigma_j.
-    double ld = l;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      double sg = (!A.mats && A.sdiag) ? A.sdiag[(int64_t)d * A.N + s[j]] : 1.0;
-      if (!A.mats && A.sdiag) ld += log(sg);
-      if (A.invdiag) {
-        double v = cs[j] / sg;
-        if (A.inv_n > 0)
-          A.invdiag[o * A.inv_n + s[j]] = v;
-        else
-          A.invdiag[o * K + j] = v;
-      }
-    }
-    if (A.logdet) A.logdet[o] = ld;
-  }
-}
-
-template <int KT, bool FIXED>
-__global__ void __launch_bounds__(128) k_eval(const EvalArgs A, int kdyn) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= A.B * A.D) return;
-  const int64_t b = t / A.D;
-  const int d = (int)(t - b * A.D);
-  eval_unit<KT, FIXED>(A, b, d, kdyn);
-}
-
-template <int KT, bool FIXED>
-static int launch_one(const EvalArgs &A, int K, cudaStream_t s) {
-  int64_t n = A.B * (int64_t)A.D;
-  if (n == 0) return HOI_OK;
-  k_eval<KT, FIXED><<<grid_for(n, 128), 128, 0, s>>>(A, K);
-  return check_launch("k_eval");
-}
-
 int launch_eval(const EvalArgs &A, int K, cudaStream_t s) {
-  switch (K) {
-#define HOI_CASE(k) \
-  case k:           \
-    return launch_one<k, true>(A, K, s);
-    HOI_CASE(1) HOI_CASE(2) HOI_CASE(3) HOI_CASE(4) HOI_CASE(5) HOI_CASE(6)
-    HOI_CASE(7) HOI_CASE(8) HOI_CASE(9) HOI_CASE(10) HOI_CASE(11) HOI_CASE(12)
-#undef HOI_CASE
-    default:
-      break;
-  }
-  if (K <= 16) return launch_one<16, false>(A, K, s);
-  if (K <= 24) return launch_one<24, false>(A, K, s);
-  if (K <= 32) return launch_one<32, false>(A, K, s);
-  if (K <= 48) return launch_one<48, false>(A, K, s);
-  if (K <= 64) return launch_one<64, false>(A, K, s);
-  return fail(HOI_INVALID_ARG, "order > 64 is not supported");
+  if (K < 1 || K > 64) return fail(HOI_INVALID_ARG, "order > 64 is not supported");
+  int st = -1;
+  if (K <= 12) st = launch_eval_k1_12(A, K, s);
+  else if (K <= 16) st = launch_eval_k13_16(A, K, s);
+  return st >= 0 ? st : launch_eval_generic(A, K, s);
 }
 
 // ------------------------------------------------------------ unranking --
