@@ -9,6 +9,7 @@ int launch_eval(const EvalArgs &A, int K, cudaStream_t s) {
   int st = -1;
   if (K <= 12) st = launch_eval_k1_12(A, K, s);
   else if (K <= 16) st = launch_eval_k13_16(A, K, s);
+  else if (K <= 32) st = launch_eval_warp(A, K, s);
   return st >= 0 ? st : launch_eval_generic(A, K, s);
 }
 

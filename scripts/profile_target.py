@@ -34,11 +34,12 @@ def main(mode):
         batch = hoi.NpletBatch(400, indices=idx, check_unique=False)
         for _ in range(2):
             hoi.compute_hoi_batch(covs, batch)
-    elif mode == "eval16":
+    elif mode in ("eval16", "eval20"):
         import math
+        k = int(mode[4:])
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
-        ctx = _ScanCtx(covs, 16, 16, False, 1)
-        n = math.comb(30, 16) // 16
+        ctx = _ScanCtx(covs, k, k, False, 1)
+        n = math.comb(30, k) // 16
         out = torch.empty((4, n, 1), dtype=torch.float64, device="cuda")
         for _ in range(2):
             ctx.full(0, n, out)
