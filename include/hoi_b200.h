@@ -179,6 +179,20 @@ int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, const double
                          int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
                          int64_t g_end, double *out, void *stream);
 
+/* Filtered stencil (scan with a TopK reducer, ref:scanner.py:50-105):
+ * the engine-2 stencil over every n-plet of orders kmin..kmax of dataset d
+ * (or over every `every`-th table block, a sample) that writes, instead of
+ * the full output, the n-plets whose key sign * measure[m_idx] (m_idx:
+ * 0 tc, 1 dtc, 2 o, 3 s) has an order-preserving 64-bit form <= *key_max
+ * (device), as 40-byte records {global rank (int64 bits), tc, dtc, o, s}
+ * appended to cand.  *count (device uint64, caller zeroes) counts every
+ * match even past cand_cap.  The table of dataset d must be built
+ * (hoi_lattice_table + hoi_lattice_status).  Asynchronous. */
+int hoi_lattice_filter(void *ws, int32_t N, int32_t D, int32_t d, const double *eta,
+                       int32_t kstride, int32_t kmin, int32_t kmax, int32_t m_idx,
+                       double sign, int32_t every, const uint64_t *key_max, double *cand,
+                       int64_t cand_cap, uint64_t *count, void *stream);
+
 /* Engine 3: both phases in ONE persistent pass (dataset d).  Warps claim
  * table blocks in increasing order, build and publish their block, then
  * acquire their (lower-index, already claimed) neighbour blocks and write
@@ -202,6 +216,13 @@ int hoi_lattice_fused(const double *corr, int32_t N, int32_t D, int32_t d, const
 int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
                     int64_t k, int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
                     int64_t *h_count, void *ws, void *stream);
+
+/* Exact k-th smallest key: the order-preserving 64-bit key of the k-th
+ * smallest sign*vals[p*D+d] over p < n (full radix select), written to
+ * device memory *key_out; all-ones when n <= k.  Synchronous.  ws: device
+ * workspace of at least 4096 uint64. */
+int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
+                       int64_t k, uint64_t *key_out, void *ws, void *stream);
 
 /* Candidate filter for TopK: writes the positions p in [0, n) of plane
  * `vals` (stride D, dataset d) whose key sign*vals[p*D+d] <= *thresh into

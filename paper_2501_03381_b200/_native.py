@@ -46,12 +46,15 @@ _SIGS = {
                        _vp, _i32, _vp, C.POINTER(_sz), _vp], C.c_int),
     "hoi_lattice_table": ([_vp, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
     "hoi_lattice_status": ([_vp, _i32, _vp], C.c_int),
+    "hoi_lattice_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _dbl, _i32, _vp,
+                            _vp, _i64, _vp, _vp], C.c_int),
     "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,
                               _vp], C.c_int),
     "hoi_lattice_fused": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp, _vp,
                            _sz, _vp], C.c_int),
     "hoi_topk_select": ([_vp, _i64, _i32, _i32, _dbl, _i64, _i64, _vp, _i64, C.POINTER(_i64),
                          _vp, _vp], C.c_int),
+    "hoi_topk_threshold": ([_vp, _i64, _i32, _i32, _dbl, _i64, _vp, _vp, _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_histogram": ([_vp, _i64, _i32, _i32, _dbl, _dbl, _vp, _vp, _vp], C.c_int),
     "hoi_fp64_probe": ([_vp, _i64, _i32, _vp], C.c_int),

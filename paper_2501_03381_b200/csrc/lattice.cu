@@ -398,6 +398,18 @@ __device__ __forceinline__ int64_t run_base(unsigned P, int q, int N, int kmin, 
   return order_off[k - kmin] + (int64_t)r - g_begin;
 }
 
+// A pseudo-random 1/every of the table blocks (the sampled pass of a
+// filtered TopK scan): a Fibonacci hash of P, high bits.  (P % every == 0
+// would keep only subsets that avoid the low prefix variables: a biased
+// sample, whose k-th key bounds the global one far more loosely.)
+__global__ void k_block_sample(unsigned nblocks, unsigned every, uint8_t *__restrict__ active) {
+  const unsigned P = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P < nblocks) {
+    const unsigned h = P * 2654435761u;
+    active[P] = (((uint64_t)h * every) >> 32) == 0 ? 1 : 0;
+  }
+}
+
 // 1 if table block P has at least one output row in [g_begin, g_end).
 __global__ void k_block_active(int N, int kmin, int kmax, const int64_t *__restrict__ order_off,
                                int64_t g_begin, int64_t g_end, unsigned nblocks,
@@ -441,13 +453,26 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 // after the only per-block barrier (named, consumers only; nbs/base are
 // double-buffered) -- writes the four measures of each run (P, q) as one
 // coalesced, contiguous span of the order-major lexicographic output.
-template <int kRing, int kMinCtas>
+// Filter mode (scan with a TopK reducer): instead of the 32 B/n-plet output,
+// emit only the n-plets whose key sign * measure[m_idx] is <= *key_max, as
+// 40-byte records (global rank as int64 bits, tc, dtc, o, s), appended with
+// one atomic per warp.  `count` keeps counting past `cap` (overflow check).
+struct StencilFilter {
+  int m_idx;
+  double sign;
+  const uint64_t *key_max;
+  double *cand;
+  unsigned long long *count;
+  int64_t cap;
+};
+
+template <int kRing, int kMinCtas, bool FILTER>
 __global__ void __launch_bounds__(kStencilThreads + 32, kMinCtas)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
                    unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
-                   int near_bits, unsigned *__restrict__ counter, int own_last) {
+                   int near_bits, unsigned *__restrict__ counter, int own_last, StencilFilter flt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StencilSmem<kRing> &sm = *reinterpret_cast<StencilSmem<kRing> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
@@ -512,6 +537,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
   const double e1 = et ? et[1] : 0.0;
   const int64_t rows = g_end - g_begin;
+  const uint64_t key_max = FILTER ? *flt.key_max : 0ull;
   // Each thread owns PAIRS entry pairs (e, e+1), e = 2*pi, pi = tid + 256 r.
   // swz(e+1) == swz(e) ^ 1, so a pair is one aligned 16-byte word whose
   // halves are swapped when bit 5 of e is set (flip): every neighbour block
@@ -578,30 +604,56 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       const uint32_t w = sm.run[tid + kStencilThreads * r];
       const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
       const int64_t b0 = sm.base[buf][q];
-      if (b0 == kNoRun) continue;
       const int k = kP + q;
       const int64_t row = b0 + t;
-      if (row < 0 || row >= rows) continue;
-      const double l = own[swz(e)], nb = nbs[swz(e)];
-      const double kd = (double)k;
-      double tc, dtc, o;
-      if (et) {
-        const double ek = et[k], ek1 = et[k - 1];
-        tc = -0.5 * l - kd * e1 + ek;
-        dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
-        o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
-      } else {
-        tc = -0.5 * l;
-        dtc = 0.5 * ((1.0 - kd) * l + nb);
-        o = 0.5 * ((kd - 2.0) * l - nb);
+      const bool valid = b0 != kNoRun && row >= 0 && row < rows;
+      double tc = 0.0, dtc = 0.0, o = 0.0;
+      if (valid) {
+        const double l = own[swz(e)], nb = nbs[swz(e)];
+        const double kd = (double)k;
+        if (et) {
+          const double ek = et[k], ek1 = et[k - 1];
+          tc = -0.5 * l - kd * e1 + ek;
+          dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
+          o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+        } else {
+          tc = -0.5 * l;
+          dtc = 0.5 * ((1.0 - kd) * l + nb);
+          o = 0.5 * ((kd - 2.0) * l - nb);
+        }
       }
-      // streaming (evict-first) stores: the 32 B/n-plet output must not
-      // push the log-det table's neighbour blocks out of L2
-      const int64_t oi = row * D + d;
-      __stcs(out + oi, tc);
-      __stcs(out + plane + oi, dtc);
-      __stcs(out + 2 * plane + oi, o);
-      __stcs(out + 3 * plane + oi, tc + dtc);
+      const double sv = tc + dtc;
+      if (!FILTER) {
+        if (valid) {
+          // streaming (evict-first) stores: the 32 B/n-plet output must not
+          // push the log-det table's neighbour blocks out of L2
+          const int64_t oi = row * D + d;
+          __stcs(out + oi, tc);
+          __stcs(out + plane + oi, dtc);
+          __stcs(out + 2 * plane + oi, o);
+          __stcs(out + 3 * plane + oi, sv);
+        }
+      } else {
+        const double v = flt.m_idx == 0 ? tc : flt.m_idx == 1 ? dtc : flt.m_idx == 2 ? o : sv;
+        const bool keep = valid && orderable_key(flt.sign * v) <= key_max;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal) {
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(flt.count, (unsigned long long)__popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (keep) {
+            const unsigned long long slot = base + __popc(bal & ((1u << lane) - 1u));
+            if ((int64_t)slot < flt.cap) {
+              double *rec = flt.cand + 5 * slot;
+              rec[0] = __longlong_as_double(row + g_begin);
+              rec[1] = tc;
+              rec[2] = dtc;
+              rec[3] = o;
+              rec[4] = sv;
+            }
+          }
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);  // own slot free
@@ -987,21 +1039,22 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   return acc;
 }
 
-template <int R, int C>
+template <int R, int C, bool F>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                        int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
-                       int near_bits, int own_last, int per_sm_cap, cudaStream_t s) {
+                       int near_bits, int own_last, int per_sm_cap, const StencilFilter &flt,
+                       cudaStream_t s) {
   static thread_local int set_for = -1;
   static thread_local int grid_cap = 0, n_sms = 0, max_per_sm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   const int smem = (int)sizeof(StencilSmem<R>);
   if (set_for != dev) {
-    cudaFuncSetAttribute(k_lattice_measures<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_lattice_measures<R, C, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C, F>,
                                                   kStencilThreads + 32, smem);
     max_per_sm = per_sm > 0 ? per_sm : 1;
     n_sms = sms;
@@ -1013,9 +1066,9 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
   if (per_sm_cap > 0 && per_sm_cap < max_per_sm) cap = (unsigned)(n_sms * per_sm_cap);
   const unsigned grid = n < cap ? n : cap;
   if (grid == 0) return HOI_OK;
-  k_lattice_measures<R, C><<<grid, kStencilThreads + 32, smem, s>>>(
+  k_lattice_measures<R, C, F><<<grid, kStencilThreads + 32, smem, s>>>(
       w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
-      blk_end, active, near_bits, w.counter, own_last);
+      blk_end, active, near_bits, w.counter, own_last, flt);
   return check_launch("k_lattice_measures");
 }
 
@@ -1026,7 +1079,8 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
 static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                           int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                           unsigned blk_begin, unsigned blk_end, int near_bits, bool partial,
-                          bool flags_ready, cudaStream_t s, int per_sm_cap = 0) {
+                          bool flags_ready, cudaStream_t s, int per_sm_cap = 0,
+                          const StencilFilter *flt = nullptr) {
   const unsigned nblocks = 1u << (N - CB);
   uint8_t *active = partial ? reinterpret_cast<uint8_t *>(w.ready) : nullptr;
   if (partial && !flags_ready) {
@@ -1036,21 +1090,26 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     if (st) return st;
   }
   // experiment knobs (defaults are the measured best)
-  // measured on B200 (cfg4): 4 CTAs x 4-slot rings beat 3 x 6 and 2 x 10
-  // (more independent in-order streams per SM), own block evict_last
+  // measured on B200 (cfg4): 4 CTAs x 4-slot rings beat 3 x 6 (17.8 ms) and
+  // 2 x 10 (20.7 ms) -- more independent in-order streams per SM; own block
+  // evict_last
   static const int ring = getenv("HOI_RING") ? atoi(getenv("HOI_RING")) : 4;
   static const int own_last = getenv("HOI_OWN_LAST") ? atoi(getenv("HOI_OWN_LAST")) : 1;
   if (getenv("HOI_NEAR_BITS")) near_bits = atoi(getenv("HOI_NEAR_BITS"));
   const int64_t plane = (g_end - g_begin) * (int64_t)D;
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
-  if (ring == 10)
-    return run_stencil<10, 2>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                              blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
-  if (ring == 4)
-    return run_stencil<4, 4>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                             blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
-  return run_stencil<6, 3>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
-                           blk_begin, blk_end, active, near_bits, own_last, per_sm_cap, s);
+  if (flt)
+    return run_stencil<4, 4, true>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                                   plane, blk_begin, blk_end, active, near_bits, own_last,
+                                   per_sm_cap, *flt, s);
+  const StencilFilter none{};
+  if (ring == 6)
+    return run_stencil<6, 3, false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                                    plane, blk_begin, blk_end, active, near_bits, own_last,
+                                    per_sm_cap, none, s);
+  return run_stencil<4, 4, false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                                  plane, blk_begin, blk_end, active, near_bits, own_last,
+                                  per_sm_cap, none, s);
 }
 
 
@@ -1065,6 +1124,31 @@ int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstri
   const bool partial = g_begin > 0 || g_end < total;
   return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, 0u,
                         1u << (N - CB), default_near_bits(N - CB), partial, false, s);
+}
+
+// Filtered stencil over the whole rank space of [kmin, kmax] (or every
+// `every`-th table block): candidates with key <= *key_max (see
+// StencilFilter).  The table must be complete (lattice_table + status).
+int lattice_filter(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
+                   int kmax, int m_idx, double sign, unsigned every, const uint64_t *key_max,
+                   double *cand, int64_t cand_cap, unsigned long long *count, cudaStream_t s) {
+  upload_binomials();
+  upload_tables();
+  LatticeWs w = ws_view(ws, N);
+  int64_t h_off[MAXV + 1];
+  const int64_t total = total_rows(N, kmin, kmax, h_off);
+  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  const unsigned nblocks = 1u << (N - CB);
+  bool sampled = every > 1;
+  if (sampled) {
+    k_block_sample<<<(nblocks + 255) / 256, 256, 0, s>>>(nblocks, every,
+                                                         reinterpret_cast<uint8_t *>(w.ready));
+    int st = check_launch("k_block_sample");
+    if (st) return st;
+  }
+  StencilFilter f{m_idx, sign, key_max, cand, count, cand_cap};
+  return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, nullptr, 0u, nblocks,
+                        default_near_bits(N - CB), sampled, sampled, s, 0, &f);
 }
 
 // Two-stream pipeline over chunks of 2^w table blocks: the table of chunk
@@ -1213,6 +1297,20 @@ extern "C" int hoi_lattice_measures(void *ws, int32_t N, int32_t D, int32_t d, c
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_measures: bias table too short");
   return lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
                           (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_filter(void *ws, int32_t N, int32_t D, int32_t d, const double *eta,
+                                  int32_t kstride, int32_t kmin, int32_t kmax, int32_t m_idx,
+                                  double sign, int32_t every, const uint64_t *key_max,
+                                  double *cand, int64_t cand_cap, uint64_t *count, void *stream) {
+  HOI_CHECK_ARG(ws && key_max && cand && count && lattice_supports(N) && d >= 0 && d < D &&
+                    kmin >= 1 && kmin <= kmax && kmax <= N && m_idx >= 0 && m_idx < 4 &&
+                    every >= 1 && cand_cap >= 0,
+                "hoi_lattice_filter: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_filter: bias table too short");
+  return lattice_filter(ws, N, D, d, eta, kstride, kmin, kmax, m_idx, sign, (unsigned)every,
+                        key_max, cand, cand_cap, reinterpret_cast<unsigned long long *>(count),
+                        (cudaStream_t)stream);
 }
 
 extern "C" int hoi_lattice_status(void *ws, int32_t N, void *stream) {

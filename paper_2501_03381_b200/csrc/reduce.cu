@@ -187,6 +187,49 @@ extern "C" int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t
   return HOI_OK;
 }
 
+// The exact k-th smallest orderable key of sign*vals[p*D+d], p < n (full
+// 64-bit radix select), written to device memory *key_out; ~0 when n <= k
+// (every element qualifies).  Synchronous.
+extern "C" int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
+                                  int64_t k, uint64_t *key_out, void *ws, void *stream) {
+  HOI_CHECK_ARG(vals && key_out && ws && d >= 0 && d < D && k >= 1 && n >= 0,
+                "hoi_topk_threshold: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
+  std::vector<unsigned long long> h(kRadixBins);
+  uint64_t prefix = 0, hi_mask = 0;
+  uint64_t key = ~0ull;
+  int64_t need = k;
+  if (n > k) {
+    const int blocks = 4 * sm_count();
+    for (int shift = 64 - kRadixBits; shift > -kRadixBits; shift -= kRadixBits) {
+      const int sh = shift < 0 ? 0 : shift;
+      const int bits = shift < 0 ? kRadixBits + shift : kRadixBits;
+      cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kRadixBins, s);
+      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, counts);
+      int st = check_launch("k_radix_hist");
+      if (st) return st;
+      cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * kRadixBins,
+                      cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      int64_t acc = 0;
+      int b = 0;
+      for (; b < (1 << bits); ++b) {
+        if (acc + (int64_t)h[b] >= need) break;
+        acc += (int64_t)h[b];
+      }
+      need -= acc;
+      prefix |= (uint64_t)b << sh;
+      hi_mask |= (uint64_t)((1 << bits) - 1) << sh;
+      if (sh == 0) break;
+    }
+    key = prefix;
+  }
+  cudaMemcpyAsync(key_out, &key, sizeof(key), cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  return HOI_OK;
+}
+
 extern "C" int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
                                const double *thresh, int64_t *cand, int64_t *cand_count,
                                int64_t cand_cap, void *stream) {

@@ -407,8 +407,8 @@ def _unrank_list(n, lo, hi, ranks):
     orders = torch.empty(m, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().hoi_unrank_list(n, lo, hi, r.data_ptr(), m, idx.data_ptr(),
                                         orders.data_ptr(), nat.stream_handle(torch)), "unrank_list")
-    hi_idx, ho = idx.cpu().numpy(), orders.cpu().numpy()
-    return [tuple(int(v) for v in hi_idx[i, :ho[i]]) for i in range(m)]
+    hi_idx, ho = idx.cpu().numpy().tolist(), orders.cpu().numpy().tolist()
+    return [tuple(row[:k]) for row, k in zip(hi_idx, ho)]
 
 
 def _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0):
@@ -520,8 +520,97 @@ def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
     reducer._merge(d, sub._best[0])
 
 
+def _topk_lattice(ctx, reducer, m_idx):
+    """TopK over an exhaustive scan without writing the full output (lattice
+    engine): per dataset, (1) build the log-det table; (2) run the filtered
+    stencil over every 256th table block with no threshold and take the
+    exact k-th smallest key of that sample -- any subset's k-th smallest
+    key bounds the global k-th smallest from above, so every true top-k
+    n-plet passes it; (3) one filtered stencil pass over all blocks keeps
+    only the n-plets at or under that key; (4) an exact radix select over
+    those candidates hands the k best (plus every tie at the k-th key) to
+    the reference's host merge (sign*value, index tuple).  Returns False
+    when the engine declines (not PD) or the sample is smaller than k; the
+    caller then takes the full-output path."""
+    torch, lib = ctx.torch, nat.lib()
+    s = nat.stream_handle(torch)
+    n = ctx.n
+    kst = 0 if ctx.eta is None else ctx.eta.shape[1]
+    k, sign = reducer.k, reducer.sign
+    nblocks = 1 << (n - 10)
+    every = 256 if nblocks >= (1 << 14) else 1
+    ws_sel = torch.empty(4096 + 64, dtype=torch.int64, device="cuda")
+    key = torch.empty(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    best = [[] for _ in range(ctx.d)]
+    for d in range(ctx.d):
+        rc = lib.hoi_lattice_table(ctx.st.corr.data_ptr(), n, ctx.d, d, ctx.ws.data_ptr(),
+                                   ctx.ws.numel(), s)
+        nat.check(rc, "lattice_table")
+        rc = lib.hoi_lattice_status(ctx.ws.data_ptr(), n, s)
+        if rc == nat.FALLBACK:
+            return False
+        nat.check(rc, "lattice_status")
+
+        def filt(every_, cap):
+            cand = torch.empty((max(cap, 1), 5), dtype=torch.float64, device="cuda")
+            cnt.zero_()
+            nat.check(lib.hoi_lattice_filter(ctx.ws.data_ptr(), n, ctx.d, d, nat.ptr(ctx.eta), kst,
+                                             ctx.lo, ctx.hi, m_idx, sign, every_, key.data_ptr(),
+                                             cand.data_ptr(), cap, cnt.data_ptr(), s),
+                      "lattice_filter")
+            return cand, int(cnt.item())
+
+        key.fill_(-1)                                   # all-ones key: no threshold
+        if every > 1:
+            cap = (nblocks // every + 1) * 1024         # every row of the sampled blocks
+            cand, c = filt(every, cap)
+            if c <= k:
+                return False
+            nat.check(lib.hoi_topk_threshold(cand.data_ptr(), c, 5, 1 + m_idx, sign, k,
+                                             key.data_ptr(), ws_sel.data_ptr(), s),
+                      "topk_threshold")
+            del cand
+            cap = max(16 * every * k, 1 << 20)
+        else:
+            cap = count_nplets(n, ctx.lo, ctx.hi)
+        cand, c = filt(1, cap)
+        if c > cap:                                     # loose sample: exact size, once more
+            cand, c = filt(1, c)
+        # exact k best (+ ties at the k-th key) among the candidates
+        sel_cap = 2 * k + 4096 + 1
+        pos = torch.empty(sel_cap, dtype=torch.int64, device="cuda")
+        hc = ctypes.c_int64(0)
+        nat.check(lib.hoi_topk_select(cand.data_ptr(), c, 5, 1 + m_idx, sign, k, k + 4096,
+                                      pos.data_ptr(), sel_cap, ctypes.byref(hc),
+                                      ws_sel.data_ptr(), s), "topk_select")
+        h = int(hc.value)
+        if h > sel_cap:                                 # a tie wider than the buffer
+            pos = torch.arange(c, device="cuda")
+            h = c
+        rec = cand[pos[:h]].cpu().numpy()
+        ranks = rec[:, 0].view(np.int64)
+        tuples = _unrank_list(n, ctx.lo, ctx.hi, ranks) if h else []
+        mv = rec[:, 1 + m_idx]
+        for i in range(h):
+            e = TopEntry(indices=tuples[i], order=len(tuples[i]), value=float(mv[i]),
+                         tc=float(rec[i, 1]), dtc=float(rec[i, 2]), o=float(rec[i, 3]),
+                         s=float(rec[i, 4]))
+            best[d].append(((sign * e.value, e.indices), e))
+    if reducer._best is None:
+        reducer._best = [[] for _ in range(ctx.d)]
+    for d in range(ctx.d):
+        reducer._merge(d, best[d])
+    ctx._table_ok = ctx.d == 1
+    return True
+
+
 def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):
     torch = ctx.torch
+    if isinstance(reducer, TopK) and ctx.engine == 2 and _topk_lattice(
+            ctx, reducer, MEASURES.index(reducer.measure)):
+        _emit_progress(progress, ctx.n, ctx.lo, ctx.hi, batch_size, total, t0)
+        return
     per_chunk = _chunk_rows(ctx.d, torch)
     hist_counts = None
     if isinstance(reducer, Histogram):

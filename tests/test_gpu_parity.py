@@ -403,3 +403,27 @@ def test_lattice_declines_singular_covariance(oracle):
     rows = [c for k in range(2, 5) for c in itertools.combinations(range(12), k)]
     clean = np.array([not (10 in r and 11 in r) for r in rows])
     np.testing.assert_allclose(got[:, clean], vals[:, clean], rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("measure,direction,k,bias", [("o", "min", 1000, False),
+                                                      ("s", "max", 100, True),
+                                                      ("tc", "max", 7, False)])
+def test_filtered_topk_matches_full_output(measure, direction, k, bias):
+    """The lattice engine's filtered TopK (sampled threshold, no full output)
+    returns exactly what the full-output path returns (itself checked against
+    the oracle above): N = 24 is the smallest size that takes the sampled
+    branch (2^14 table blocks), orders 2..24, 16.8M n-plets."""
+    from paper_2501_03381_b200 import scanner
+    rng = np.random.default_rng(7)
+    c = workloads.randcorr(24, rng)
+    x = rng.standard_normal((3000, 24)) @ np.linalg.cholesky(c).T
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
+    got = hoi.scan(covs, 2, 24, hoi.TopK(measure, direction, k), bias_correct=bias)[0]
+    ctx = scanner._ScanCtx(covs, 2, 24, bias, 2)
+    ref = hoi.TopK(measure, direction, k)
+    total = hoi.count_nplets(24, 2, 24)
+    out, _, _ = ctx.full(0, total)
+    scanner._topk_plane(ctx, ref, out, 0, scanner.MEASURES.index(measure))
+    want = ref.finalize()[0]
+    assert [e.indices for e in got] == [e.indices for e in want]
+    assert [(e.tc, e.dtc, e.o, e.s) for e in got] == [(e.tc, e.dtc, e.o, e.s) for e in want]
