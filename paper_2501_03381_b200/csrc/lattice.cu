@@ -466,22 +466,80 @@ struct StencilFilter {
   int64_t cap;
 };
 
-template <int kRing, int kMinCtas, bool FILTER>
+// Pass configuration of the stencil (see the two-pass split in DESIGN.md):
+//   nbmask  prefix bits whose neighbour blocks T[P ^ 2^j] are streamed;
+//   extra   if set, block P of this array (the partial sums of the low
+//           pass) is streamed and added like a neighbour;
+//   sums    MODE_LOWSUM: where the neighbour sums are written (T layout);
+//   perm_lb claim order: 0 = natural, else the high nP-perm_lb bits vary
+//           fastest (so the streamed high-bit neighbours are recent).
+//   list    if set, the blocks to process in claim order (*nlist of them):
+//           the compacted active blocks of a partial or sampled scan.
+struct StencilPass {
+  unsigned nbmask;
+  const double *extra;
+  double *sums;
+  int perm_lb;
+  const unsigned *list;
+  const unsigned *nlist;
+};
+
+// Compact the flagged blocks into a list in claim order (natural, or
+// high-bits-fastest when perm_lb > 0).  One CTA of 1024 threads: each
+// thread counts a contiguous slice of claim indices, a block scan gives its
+// write offset.  Skipping inactive blocks one atomic claim at a time costs
+// every producer ~nblocks/active serialized atomics per block it keeps.
+__global__ void __launch_bounds__(1024)
+k_compact_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb,
+                 unsigned *__restrict__ list, unsigned *__restrict__ count) {
+  __shared__ unsigned part[1024];
+  const unsigned n = 1u << nP, t = threadIdx.x;
+  const unsigned per = (n + 1023) / 1024, c0 = t * per, c1 = c0 + per < n ? c0 + per : n;
+  const int hb = nP - perm_lb;
+  auto perm = [&](unsigned c) {
+    return perm_lb ? (((c & ((1u << hb) - 1u)) << perm_lb) | (c >> hb)) : c;
+  };
+  unsigned cnt = 0;
+  for (unsigned c = c0; c < c1; ++c) cnt += active[perm(c)];
+  part[t] = cnt;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {       // inclusive Hillis-Steele scan
+    const unsigned v = t >= (unsigned)o ? part[t - o] : 0u;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  unsigned pos = part[t] - cnt;
+  for (unsigned c = c0; c < c1; ++c) {
+    const unsigned q = perm(c);
+    if (active[q]) list[pos++] = q;
+  }
+  if (t == 1023) *count = part[1023];
+}
+
+enum { MODE_FULL = 0, MODE_FILTER = 1, MODE_LOWSUM = 2 };
+
+template <int kRing, int kMinCtas, int MODE>
 __global__ void __launch_bounds__(kStencilThreads + 32, kMinCtas)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
                    unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
-                   int near_bits, unsigned *__restrict__ counter, int own_last, StencilFilter flt) {
+                   int near_bits, unsigned *__restrict__ counter, int own_last, StencilFilter flt,
+                   StencilPass ps) {
+  constexpr bool FILTER = MODE == MODE_FILTER;
+  constexpr bool OWN = MODE != MODE_LOWSUM;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StencilSmem<kRing> &sm = *reinterpret_cast<StencilSmem<kRing> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int p = tid; p < BLK; p += blockDim.x) {
-    const int e = __ldg(g_runmask + p);
-    const int q = __popc(e);
-    sm.run[p] = (uint32_t)e | ((uint32_t)(p - c_runstart[q]) << 10) | ((uint32_t)q << 20);
+  if (OWN) {
+    for (int p = tid; p < BLK; p += blockDim.x) {
+      const int e = __ldg(g_runmask + p);
+      const int q = __popc(e);
+      sm.run[p] = (uint32_t)e | ((uint32_t)(p - c_runstart[q]) << 10) | ((uint32_t)q << 20);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < kRing; ++s) {
@@ -491,24 +549,35 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const unsigned nbmask = ps.nbmask;
+  const int nP = N - CB;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------ producer ----
     if (lane != 0) return;
     const uint64_t pol_near = l2_policy(false), pol_far = l2_policy(true);
     const uint64_t pol_own = own_last ? l2_policy_last() : pol_near;
+    const int hb = nP - ps.perm_lb;
     uint32_t pJ = 0;
     for (uint32_t seq = 0;; ++seq) {
       unsigned P = kEndBlock;
-      for (;;) {
+      if (ps.list) {
         const unsigned c = atomicAdd(counter, 1u);
-        if (c >= blk_end - blk_begin) break;
-        if (!active || active[blk_begin + c]) {
-          P = blk_begin + c;
-          break;
+        if (c < *ps.nlist) P = ps.list[c];
+      } else {
+        for (;;) {
+          const unsigned c = atomicAdd(counter, 1u);
+          if (c >= blk_end - blk_begin) break;
+          const unsigned q = ps.perm_lb ? (((c & ((1u << hb) - 1u)) << ps.perm_lb) | (c >> hb)) : c;
+          if (!active || active[blk_begin + q]) {
+            P = blk_begin + q;
+            break;
+          }
         }
       }
-      unsigned prem = P == kEndBlock ? 0u : P;
+      unsigned prem = P == kEndBlock ? 0u : (P & nbmask);
+      // jobs of P: neighbours (far bits first), the partial-sum block, the own block
+      int stage = prem ? 0 : (ps.extra ? 1 : (OWN ? 2 : 3));
       for (bool first = true;; first = false) {
         const int slot = pJ % kRing;
         if (pJ >= kRing) mbar_wait(&sm.empty[slot], ((pJ / kRing) - 1) & 1u);
@@ -517,18 +586,30 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
           mbar_arrive(&sm.full[slot]);             // tx-free arrival: the end marker
           return;
         }
-        unsigned src = P;
-        uint64_t pol = pol_own;
-        if (prem) {
+        const double *srcp;
+        uint64_t pol = pol_near;
+        if (stage == 0) {
           const int j = 31 - __clz(prem);
           prem &= ~(1u << j);
-          src = P ^ (1u << j);
+          srcp = table + (int64_t)(P ^ (1u << j)) * BLK;
           pol = j >= near_bits ? pol_far : pol_near;
+          if (!prem) stage = ps.extra ? 1 : (OWN ? 2 : 4);
+        } else if (stage == 1) {
+          srcp = ps.extra + (int64_t)P * BLK;
+          stage = OWN ? 2 : 4;
+        } else if (stage == 2) {
+          srcp = table + (int64_t)P * BLK;
+          pol = pol_own;
+          stage = 4;
+        } else {                                   // stage 3: a block with no job at all
+          mbar_arrive(&sm.full[slot]);
+          ++pJ;
+          break;
         }
         mbar_expect_tx(&sm.full[slot], kBlkBytes);
-        tma_load_1d(sm.ring[slot], table + (int64_t)src * BLK, kBlkBytes, &sm.full[slot], pol);
+        tma_load_1d(sm.ring[slot], srcp, kBlkBytes, &sm.full[slot], pol);
         ++pJ;
-        if (src == P) break;                       // own block issued: block complete
+        if (stage == 4) break;                     // block complete
       }
     }
   }
@@ -558,11 +639,12 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const unsigned P = *(volatile unsigned *)&blkq[seq % kBlkQ];
     if (P == kEndBlock) break;
     const int kP = __popc(P);
-    if (tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
+    const int nj = __popc(P & nbmask) + (ps.extra ? 1 : 0);
+    if (OWN && tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
     double2 acc[PAIRS];
 #pragma unroll
     for (int r = 0; r < PAIRS; ++r) acc[r] = make_double2(0.0, 0.0);
-    for (int m = 0; m < kP; ++m, ++J) {
+    for (int m = 0; m < nj; ++m, ++J) {
       const int slot = J % kRing;
       mbar_wait(&sm.full[slot], (J / kRing) & 1u);
       const double *src = sm.ring[slot];
@@ -574,6 +656,18 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    }
+    if (!OWN) {
+      // low pass: the neighbour sums of P, in the table's (swizzled) layout
+      if (nj == 0) {                               // the zero job that carried P
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[J % kRing]);
+        ++J;
+      }
+      double *dst = ps.sums + (int64_t)P * BLK;
+#pragma unroll
+      for (int r = 0; r < PAIRS; ++r) __stcg(reinterpret_cast<double2 *>(dst + pw[r]), acc[r]);
+      continue;
     }
     const int slot = J % kRing;
     mbar_wait(&sm.full[slot], (J / kRing) & 1u);
@@ -642,9 +736,9 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
           if (lane == 0) base = atomicAdd(flt.count, (unsigned long long)__popc(bal));
           base = __shfl_sync(0xffffffffu, base, 0);
           if (keep) {
-            const unsigned long long slot = base + __popc(bal & ((1u << lane) - 1u));
-            if ((int64_t)slot < flt.cap) {
-              double *rec = flt.cand + 5 * slot;
+            const unsigned long long slot2 = base + __popc(bal & ((1u << lane) - 1u));
+            if ((int64_t)slot2 < flt.cap) {
+              double *rec = flt.cand + 5 * slot2;
               rec[0] = __longlong_as_double(row + g_begin);
               rec[1] = tc;
               rec[2] = dtc;
@@ -943,8 +1037,12 @@ bool lattice_supports(int N) { return N >= CB + 2 && N <= MAXV; }
 int lattice_ws_bytes(int N, int D, size_t *bytes) {
   (void)D;
   if (!lattice_supports(N)) return fail(HOI_INVALID_ARG, "lattice engine needs 12 <= N <= 32");
-  // table 2^N f64 | misc (flag, err, counter, order offsets) 4 KB | flags 2^(N-10) u32
+  // table 2^N f64 | misc (flag, err, counter, order offsets) 4 KB | flags
+  // 2^(N-10) u32 | pad to 256 B | low-pass neighbour sums 2^N f64 (N >= 24)
   *bytes = (sizeof(double) << N) + 4096 + (sizeof(unsigned) << (N - CB));
+  if (N - CB >= 14) *bytes = ((*bytes + 255) & ~(size_t)255) + (sizeof(double) << N);
+  // | compacted block lists 2 x 2^(N-10) u32 + 2 counts
+  *bytes = ((*bytes + 255) & ~(size_t)255) + (sizeof(unsigned) << (N - CB + 1)) + 64;
   return HOI_OK;
 }
 
@@ -956,6 +1054,8 @@ struct LatticeWs {
   unsigned *counter;  // fused pass: block claim counter
   int64_t *offs;      // order offsets
   unsigned *ready;    // fused pass: per-block publish flags
+  double *lowsum;     // two-pass stencil: low-bit neighbour sums (or nullptr)
+  unsigned *list;     // compacted block lists (2 x 2^(N-10)) + 2 counts
 };
 
 static LatticeWs ws_view(void *ws, int N) {
@@ -967,6 +1067,14 @@ static LatticeWs ws_view(void *ws, int N) {
   w.counter = reinterpret_cast<unsigned *>(w.flag + 8);
   w.offs = reinterpret_cast<int64_t *>(base + 64);
   w.ready = reinterpret_cast<unsigned *>(base + 4096);
+  w.lowsum = nullptr;
+  size_t off = (sizeof(double) << N) + 4096 + (sizeof(unsigned) << (N - CB));
+  off = (off + 255) & ~(size_t)255;
+  if (N - CB >= 14) {
+    w.lowsum = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + off);
+    off = (off + (sizeof(double) << N) + 255) & ~(size_t)255;
+  }
+  w.list = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(ws) + off);
   return w;
 }
 
@@ -1039,12 +1147,12 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   return acc;
 }
 
-template <int R, int C, bool F>
+template <int R, int C, int F>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                        int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
                        int near_bits, int own_last, int per_sm_cap, const StencilFilter &flt,
-                       cudaStream_t s) {
+                       const StencilPass &ps, cudaStream_t s) {
   static thread_local int set_for = -1;
   static thread_local int grid_cap = 0, n_sms = 0, max_per_sm = 0;
   int dev = 0;
@@ -1068,7 +1176,7 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
   if (grid == 0) return HOI_OK;
   k_lattice_measures<R, C, F><<<grid, kStencilThreads + 32, smem, s>>>(
       w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
-      blk_end, active, near_bits, w.counter, own_last, flt);
+      blk_end, active, near_bits, w.counter, own_last, flt, ps);
   return check_launch("k_lattice_measures");
 }
 
@@ -1097,21 +1205,62 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   static const int own_last = getenv("HOI_OWN_LAST") ? atoi(getenv("HOI_OWN_LAST")) : 1;
   if (getenv("HOI_NEAR_BITS")) near_bits = atoi(getenv("HOI_NEAR_BITS"));
   const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  const int nP = N - CB;
+  const unsigned all = (1u << nP) - 1u;
+  // Two-pass split over the whole block space (nP >= 14): pass 1 writes the
+  // sums over the low LB = nP/2 prefix bits' neighbours (natural order: they
+  // lie within 2^LB blocks); pass 2 claims blocks high-bits-fastest and
+  // streams only the high-bit neighbours (within 2^(nP-LB) blocks) plus the
+  // pass-1 sums and the own block.  Both windows are a few MB, so neighbour
+  // reads hit L2 instead of costing ~(nP - log2 L2-blocks)/2 DRAM re-reads per
+  // block; the price is one extra write + read of the table size.
+  // Measured on B200, cfg4: full output 19.25 ms two-pass vs 20.41 single
+  // (DRAM 68.8 vs 84.2 GB); the filtered (TopK) pass writes nothing and is
+  // bound by per-job TMA latency rather than bytes, so there the single pass
+  // wins (11.4 ms vs 3.4 + 9.6 ms).
+  static const int two_env = getenv("HOI_TWO_PASS") ? atoi(getenv("HOI_TWO_PASS")) : 1;
+  static const int two_flt = getenv("HOI_TWO_PASS_FILTER") ? atoi(getenv("HOI_TWO_PASS_FILTER")) : 0;
+  const bool two = (flt ? two_flt : two_env) && nP >= 14 && blk_begin == 0 &&
+                   blk_end == (1u << nP) && w.lowsum;
+  const int lb = nP / 2;
+  const StencilFilter none{};
+  StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr};
+  // partial / sampled scans over the whole block space: compacted block
+  // lists (natural order for a single pass or pass 1, high-bits-fastest for
+  // pass 2) in the workspace after the flags
+  const bool listed = active && blk_begin == 0 && blk_end == (1u << nP);
+  unsigned *list1 = w.list, *list2 = w.list + (1u << nP), *cnts = w.list + 2 * (1u << nP);
+  if (listed) {
+    k_compact_blocks<<<1, 1024, 0, s>>>(active, nP, 0, list1, cnts);
+    if (two) k_compact_blocks<<<1, 1024, 0, s>>>(active, nP, lb, list2, cnts + 1);
+    int st = check_launch("k_compact_blocks");
+    if (st) return st;
+    ps.list = list1;
+    ps.nlist = cnts;
+  }
+  if (two) {
+    StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist};
+    cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+    int st = run_stencil<4, 4, MODE_LOWSUM>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
+                                            out, plane, blk_begin, blk_end, active, near_bits,
+                                            own_last, per_sm_cap, none, p1, s);
+    if (st) return st;
+    ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
+                     listed ? cnts + 1 : nullptr};
+  }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
   if (flt)
-    return run_stencil<4, 4, true>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
-                                   plane, blk_begin, blk_end, active, near_bits, own_last,
-                                   per_sm_cap, *flt, s);
-  const StencilFilter none{};
+    return run_stencil<4, 4, MODE_FILTER>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
+                                          out, plane, blk_begin, blk_end, active, near_bits,
+                                          own_last, per_sm_cap, *flt, ps, s);
   if (ring == 6)
-    return run_stencil<6, 3, false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
-                                    plane, blk_begin, blk_end, active, near_bits, own_last,
-                                    per_sm_cap, none, s);
-  return run_stencil<4, 4, false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
-                                  plane, blk_begin, blk_end, active, near_bits, own_last,
-                                  per_sm_cap, none, s);
+    return run_stencil<6, 3, MODE_FULL>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                                        plane, blk_begin, blk_end, active, near_bits, own_last,
+                                        per_sm_cap, none, ps, s);
+  return run_stencil<4, 4, MODE_FULL>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
+                                      plane, blk_begin, blk_end, active, near_bits, own_last,
+                                      per_sm_cap, none, ps, s);
 }
-
 
 int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
                      int kmax, int64_t g_begin, int64_t g_end, double *out, cudaStream_t s) {

@@ -27,6 +27,10 @@ def main(mode):
         out = torch.empty((4, total, 1), dtype=torch.float64, device="cuda")
         for _ in range(2):
             ctx.full(0, total, out)
+    elif mode == "topk":
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
+        for _ in range(2):
+            hoi.scan(covs, 2, 30, hoi.TopK("o", "min", 1000))
     elif mode == "eval10":
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(d)))
                            for d in range(16)])
