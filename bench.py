@@ -205,8 +205,9 @@ def measured_peaks():
 def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
     """Per-kernel CUDA-event timing of the two lattice phases on the
     launching stream, repeated `steps` times; the dominant kernel is the
-    stencil/measures pass (HBM-bound: reads the 2^N log-det table, writes
-    4 x f64 per n-plet)."""
+    stencil/measures phase (HBM-bound: reads the 2^N log-det table, writes
+    4 x f64 per n-plet; two launches of k_lattice_measures, timed together
+    as hoi_lattice_measures)."""
     s = nat.stream_handle(torch)
     ws, wsb = ctx.ws, ctx.ws.numel()
     t_tab, t_mea = [], []
@@ -232,7 +233,8 @@ def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
         traffic = json.loads(tf.read_text()).get("k_lattice_measures_bytes")
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
-            "kernel": "k_lattice_measures (leave-one-out stencil + TC/DTC/O/S epilogue)",
+            "kernel": "k_lattice_measures, two passes (low-bit neighbour sums; high-bit "
+                      "neighbours + in-block stencil + TC/DTC/O/S epilogue)",
             "peak_source": src,
             "algorithmic_bytes_per_launch": alg,
             "algorithmic_bytes_note": "8 B x 2^N log-det table read once + 32 B x n-plets written",
