@@ -331,18 +331,28 @@ def b200_arm(a):
     import paper_2501_03381_b200 as hoi
     from paper_2501_03381_b200 import _build, _native as nat, workloads
     from paper_2501_03381_b200.scanner import _ScanCtx
-    from paper_2501_03381_b200.sharding import nplet_flops, rank_ranges
+    from paper_2501_03381_b200.sharding import block_shard_bits, nplet_flops, rank_ranges
     _build.build()
     lib = nat.load()
 
     x = workloads.cfg4()
     covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
-    g0, g1 = rank_ranges(N, LO, HI, world, "count" if a.engine != 1 else "flops")[rank]
     ctx = _ScanCtx(covs, LO, HI, False, a.engine)
-    out = torch.empty((4, g1 - g0, 1), dtype=torch.float64, device="cuda")
+    sb = block_shard_bits(N, world) if world > 1 and ctx.engine == 2 else None
+    if sb is not None:
+        # block shards: this rank's n-plets at their global rows of a
+        # full-size output (rows of other ranks untouched)
+        g0, g1 = 0, TOTAL
+        out = torch.empty((4, TOTAL, 1), dtype=torch.float64, device="cuda")
 
-    def step():
-        ctx.full(g0, g1, out)
+        def step():
+            ctx.full_shard(rank, sb, out)
+    else:
+        g0, g1 = rank_ranges(N, LO, HI, world, "count" if a.engine != 1 else "flops")[rank]
+        out = torch.empty((4, g1 - g0, 1), dtype=torch.float64, device="cuda")
+
+        def step():
+            ctx.full(g0, g1, out)
 
     for _ in range(a.warmup):
         step()
@@ -372,14 +382,14 @@ def b200_arm(a):
     # the launching stream (engine 1: one launch per order segment)
     engine_used = ctx.engine
     roof = None
-    if rank == 0 and engine_used == 2:
+    if rank == 0 and engine_used == 2 and sb is None:
         roof = lattice_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     if rank == 0 and engine_used == 3:
         roof = fused_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     del out
     torch.cuda.empty_cache()
     fp64 = None
-    if rank == 0 and (engine_used == 1 or not a.no_percell):
+    if rank == 0 and (engine_used == 1 or (not a.no_percell and world == 1)):
         fp64 = percell_roofline(torch, lib, nat, covs, g0, g1, ms if engine_used == 1 else None)
         if engine_used == 1:
             roof = fp64
@@ -395,7 +405,8 @@ def b200_arm(a):
                                    "full output (4 x f64 per n-plet) written to HBM",
                        "nplets": TOTAL, "engine": engine_used,
                        "l2_flush": "each step writes 34.4 GB of output (> 126 MB L2)",
-                       "parallelism": f"rank-range shards x{world}"},
+                       "parallelism": (f"lattice block shards x{world} (top {sb} prefix bits)"
+                                       if sb is not None else f"rank-range shards x{world}")},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "roofline": roof,

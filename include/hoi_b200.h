@@ -193,6 +193,28 @@ int hoi_lattice_filter(void *ws, int32_t N, int32_t D, int32_t d, const double *
                        double sign, int32_t every, const uint64_t *key_max, double *cand,
                        int64_t cand_cap, uint64_t *count, void *stream);
 
+/* Block-sharded engine-2 scan (one process per GPU, no data-path
+ * collective): shard `shard` of 2^shard_bits (shard_bits <= (N-10)/2) owns
+ * the log-det table blocks whose top shard_bits prefix-variable bits equal
+ * `shard`, i.e. every n-plet whose intersection with variables
+ * N-10-shard_bits..N-11 is that pattern.  It rebuilds only the table
+ * chunks its stencil reads (its own and the chunks with one of its bits
+ * cleared) and writes each of its n-plets at its GLOBAL row of `out`
+ * (full-size layout of hoi_scan_full over [0, total)); the shards' row sets
+ * partition the scan.  Synchronous on a non-PD table (HOI_FALLBACK).
+ * hoi_lattice_shard_filter: the same shard through the TopK filter of
+ * hoi_lattice_filter (every > 1: a hash sample of the shard's blocks;
+ * build_table = 0 reuses the chunks built by a previous call). */
+int hoi_lattice_shard(const double *corr, int32_t N, int32_t D, int32_t d, const double *eta,
+                      int32_t kstride, int32_t kmin, int32_t kmax, int32_t shard,
+                      int32_t shard_bits, double *out, void *ws, size_t ws_bytes, void *stream);
+int hoi_lattice_shard_filter(const double *corr, int32_t N, int32_t D, int32_t d,
+                             const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
+                             int32_t shard, int32_t shard_bits, int32_t every, int32_t m_idx,
+                             double sign, const uint64_t *key_max, double *cand,
+                             int64_t cand_cap, uint64_t *count, int32_t build_table, void *ws,
+                             size_t ws_bytes, void *stream);
+
 /* Engine 3: both phases in ONE persistent pass (dataset d).  Warps claim
  * table blocks in increasing order, build and publish their block, then
  * acquire their (lower-index, already claimed) neighbour blocks and write

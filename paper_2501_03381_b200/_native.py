@@ -46,6 +46,10 @@ _SIGS = {
                        _vp, _i32, _vp, C.POINTER(_sz), _vp], C.c_int),
     "hoi_lattice_table": ([_vp, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
     "hoi_lattice_status": ([_vp, _i32, _vp], C.c_int),
+    "hoi_lattice_shard": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp,
+                           _sz, _vp], C.c_int),
+    "hoi_lattice_shard_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                  _i32, _dbl, _vp, _vp, _i64, _vp, _i32, _vp, _sz, _vp], C.c_int),
     "hoi_lattice_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _dbl, _i32, _vp,
                             _vp, _i64, _vp, _vp], C.c_int),
     "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,

@@ -410,6 +410,17 @@ __global__ void k_block_sample(unsigned nblocks, unsigned every, uint8_t *__rest
   }
 }
 
+// Block shard `shard` of 2^sb: the table blocks whose top sb prefix bits
+// equal shard (optionally intersected with a hash sample, every > 1).
+__global__ void k_block_shard(unsigned nblocks, int nP, int sb, unsigned shard, unsigned every,
+                              uint8_t *__restrict__ active) {
+  const unsigned P = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P >= nblocks) return;
+  bool on = sb == 0 || (P >> (nP - sb)) == shard;
+  if (every > 1) on = on && (((uint64_t)(P * 2654435761u) * every) >> 32) == 0;
+  active[P] = on ? 1 : 0;
+}
+
 // 1 if table block P has at least one output row in [g_begin, g_end).
 __global__ void k_block_active(int N, int kmin, int kmax, const int64_t *__restrict__ order_off,
                                int64_t g_begin, int64_t g_end, unsigned nblocks,
@@ -1300,6 +1311,53 @@ int lattice_filter(void *ws, int N, int D, int d, const double *eta, int kstride
                         default_near_bits(N - CB), sampled, sampled, s, 0, &f);
 }
 
+// Block-sharded scan (multi-GPU): shard `shard` of 2^sb owns the table
+// blocks whose top sb prefix bits equal shard and computes every n-plet of
+// those blocks, written at its GLOBAL row in `out` (full-size, rows
+// [0, total)); the union over shards is the whole scan and no row is
+// written twice.  It rebuilds only the table chunks its stencil reads: its
+// own and, for every set bit t of shard, the chunk shard with t cleared
+// (neighbours only ever remove a variable).  With filter != nullptr the
+// shard's n-plets go through the TopK filter instead (every > 1: a hash
+// sample of the shard's blocks).
+int lattice_status(void *ws, int N, cudaStream_t s);
+
+int lattice_shard(const double *corr, int N, int D, int d, const double *eta, int kstride,
+                  int kmin, int kmax, int shard, int sb, unsigned every, double *out,
+                  const StencilFilter *flt, bool build, void *ws, size_t ws_bytes,
+                  cudaStream_t s) {
+  size_t need = 0;
+  int st = lattice_ws_bytes(N, D, &need);
+  if (st) return st;
+  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
+  const int nP = N - CB;
+  if (sb < 0 || sb > nP / 2 || shard < 0 || shard >= (1 << sb))
+    return fail(HOI_INVALID_ARG, "lattice_shard: need 0 <= shard < 2^sb, sb <= (N-10)/2");
+  upload_binomials();
+  upload_tables();
+  LatticeWs w = ws_view(ws, N);
+  int64_t h_off[MAXV + 1];
+  const int64_t total = total_rows(N, kmin, kmax, h_off);
+  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  const int b = nP < MAXB ? nP : MAXB;
+  const unsigned chunk_ctas = 1u << (nP - b - sb);     // table CTAs of one shard chunk
+  if (build) cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+  for (unsigned c = 0; build && c < (1u << sb); ++c) {
+    if ((c & ~(unsigned)shard) != 0) continue;         // c must be shard with some bits cleared
+    if (c != (unsigned)shard && __builtin_popcount((unsigned)shard ^ c) != 1) continue;
+    k_lattice_table<8><<<chunk_ctas, 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag,
+                                                  c * chunk_ctas);
+    if ((st = check_launch("k_lattice_table"))) return st;
+  }
+  if (build && (st = lattice_status(ws, N, s))) return st;
+  const unsigned nblocks = 1u << nP;
+  k_block_shard<<<(nblocks + 255) / 256, 256, 0, s>>>(nblocks, nP, sb, (unsigned)shard, every,
+                                                      reinterpret_cast<uint8_t *>(w.ready));
+  if ((st = check_launch("k_block_shard"))) return st;
+  return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, out, 0u, nblocks,
+                        default_near_bits(nP), true, true, s, 0, flt);
+}
+
 // Two-stream pipeline over chunks of 2^w table blocks: the table of chunk
 // c+1 is built on an auxiliary stream while the stencil consumes chunk c,
 // so a chunk's own blocks and its neighbours within distance 2^w (the
@@ -1460,6 +1518,37 @@ extern "C" int hoi_lattice_filter(void *ws, int32_t N, int32_t D, int32_t d, con
   return lattice_filter(ws, N, D, d, eta, kstride, kmin, kmax, m_idx, sign, (unsigned)every,
                         key_max, cand, cand_cap, reinterpret_cast<unsigned long long *>(count),
                         (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_shard(const double *corr, int32_t N, int32_t D, int32_t d,
+                                 const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
+                                 int32_t shard, int32_t shard_bits, double *out, void *ws,
+                                 size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && out && lattice_supports(N) && d >= 0 && d < D && kmin >= 1 &&
+                    kmin <= kmax && kmax <= N,
+                "hoi_lattice_shard: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard: bias table too short");
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard, shard_bits, 1u, out,
+                       nullptr, true, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_shard_filter(const double *corr, int32_t N, int32_t D, int32_t d,
+                                        const double *eta, int32_t kstride, int32_t kmin,
+                                        int32_t kmax, int32_t shard, int32_t shard_bits,
+                                        int32_t every, int32_t m_idx, double sign,
+                                        const uint64_t *key_max, double *cand, int64_t cand_cap,
+                                        uint64_t *count, int32_t build_table, void *ws,
+                                        size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && key_max && cand && count && lattice_supports(N) && d >= 0 &&
+                    d < D && kmin >= 1 && kmin <= kmax && kmax <= N && m_idx >= 0 && m_idx < 4 &&
+                    every >= 1,
+                "hoi_lattice_shard_filter: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_filter: bias table too short");
+  StencilFilter f{m_idx, sign, key_max, cand, reinterpret_cast<unsigned long long *>(count),
+                  cand_cap};
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard, shard_bits,
+                       (unsigned)every, nullptr, &f, build_table != 0, ws, ws_bytes,
+                       (cudaStream_t)stream);
 }
 
 extern "C" int hoi_lattice_status(void *ws, int32_t N, void *stream) {

@@ -359,6 +359,41 @@ class _ScanCtx:
         return out, cnt, coords
 
 
+    def full_shard(self, shard: int, shard_bits: int, out=None):
+        """Lattice engine, block shard `shard` of 2^shard_bits: every n-plet
+        of the shard's table blocks at its GLOBAL row of a full-size
+        (4, total, D) output (rows of other shards are left untouched)."""
+        torch, lib = self.torch, nat.lib()
+        total = count_nplets(self.n, self.lo, self.hi)
+        if out is None:
+            out = torch.empty((4, total, self.d), dtype=torch.float64, device="cuda")
+        s = nat.stream_handle(torch)
+        kst = 0 if self.eta is None else self.eta.shape[1]
+        for d in range(self.d):
+            nat.check(lib.hoi_lattice_shard(self.st.corr.data_ptr(), self.n, self.d, d,
+                                            nat.ptr(self.eta), kst, self.lo, self.hi, shard,
+                                            shard_bits, out.data_ptr(), self.ws.data_ptr(),
+                                            self.ws.numel(), s), "lattice_shard")
+        self._table_ok = False
+        return out
+
+
+def shard_rows(n: int, lo: int, hi: int, shard: int, shard_bits: int) -> np.ndarray:
+    """Global ranks owned by block shard `shard` of 2^shard_bits (host
+    model of hoi_lattice_shard's partition, for tests): the n-plets whose
+    membership pattern over variables n-10-shard_bits .. n-11 equals shard."""
+    import itertools
+    lo_var = n - 10 - shard_bits
+    rows, g = [], 0
+    for k in range(lo, hi + 1):
+        for c in itertools.combinations(range(n), k):
+            pat = sum(1 << (v - lo_var) for v in c if lo_var <= v < n - 10)
+            if pat == shard:
+                rows.append(g)
+            g += 1
+    return np.asarray(rows, dtype=np.int64)
+
+
 def scan_device(covs: CovSet, min_order: int, max_order: int, *, bias_correct: bool = False,
                 g_begin: int = 0, g_end: int | None = None, engine: int = 0,
                 out=None) -> DeviceScan:
@@ -520,7 +555,7 @@ def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
     reducer._merge(d, sub._best[0])
 
 
-def _topk_lattice(ctx, reducer, m_idx):
+def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
     """TopK over an exhaustive scan without writing the full output (lattice
     engine): per dataset, (1) build the log-det table; (2) run the filtered
     stencil over every 256th table block with no threshold and take the
@@ -531,7 +566,8 @@ def _topk_lattice(ctx, reducer, m_idx):
     those candidates hands the k best (plus every tie at the k-th key) to
     the reference's host merge (sign*value, index tuple).  Returns False
     when the engine declines (not PD) or the sample is smaller than k; the
-    caller then takes the full-output path."""
+    caller then takes the full-output path.  shard_bits > 0: only the
+    n-plets of block shard `shard` (multi-GPU; see ScanCtx.full_shard)."""
     torch, lib = ctx.torch, nat.lib()
     s = nat.stream_handle(torch)
     n = ctx.n
@@ -544,21 +580,32 @@ def _topk_lattice(ctx, reducer, m_idx):
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     best = [[] for _ in range(ctx.d)]
     for d in range(ctx.d):
-        rc = lib.hoi_lattice_table(ctx.st.corr.data_ptr(), n, ctx.d, d, ctx.ws.data_ptr(),
-                                   ctx.ws.numel(), s)
-        nat.check(rc, "lattice_table")
-        rc = lib.hoi_lattice_status(ctx.ws.data_ptr(), n, s)
-        if rc == nat.FALLBACK:
-            return False
-        nat.check(rc, "lattice_status")
+        if shard_bits == 0:
+            rc = lib.hoi_lattice_table(ctx.st.corr.data_ptr(), n, ctx.d, d, ctx.ws.data_ptr(),
+                                       ctx.ws.numel(), s)
+            nat.check(rc, "lattice_table")
+            rc = lib.hoi_lattice_status(ctx.ws.data_ptr(), n, s)
+            if rc == nat.FALLBACK:
+                return False
+            nat.check(rc, "lattice_status")
+        built = [False]
 
         def filt(every_, cap):
             cand = torch.empty((max(cap, 1), 5), dtype=torch.float64, device="cuda")
             cnt.zero_()
-            nat.check(lib.hoi_lattice_filter(ctx.ws.data_ptr(), n, ctx.d, d, nat.ptr(ctx.eta), kst,
-                                             ctx.lo, ctx.hi, m_idx, sign, every_, key.data_ptr(),
-                                             cand.data_ptr(), cap, cnt.data_ptr(), s),
-                      "lattice_filter")
+            if shard_bits == 0:
+                rc = lib.hoi_lattice_filter(ctx.ws.data_ptr(), n, ctx.d, d, nat.ptr(ctx.eta), kst,
+                                            ctx.lo, ctx.hi, m_idx, sign, every_, key.data_ptr(),
+                                            cand.data_ptr(), cap, cnt.data_ptr(), s)
+            else:
+                rc = lib.hoi_lattice_shard_filter(
+                    ctx.st.corr.data_ptr(), n, ctx.d, d, nat.ptr(ctx.eta), kst, ctx.lo, ctx.hi,
+                    shard, shard_bits, every_, m_idx, sign, key.data_ptr(), cand.data_ptr(), cap,
+                    cnt.data_ptr(), 0 if built[0] else 1, ctx.ws.data_ptr(), ctx.ws.numel(), s)
+                if rc == nat.FALLBACK:
+                    return None, -1
+                built[0] = True
+            nat.check(rc, "lattice_filter")
             return cand, int(cnt.item())
 
         key.fill_(-1)                                   # all-ones key: no threshold
@@ -575,6 +622,8 @@ def _topk_lattice(ctx, reducer, m_idx):
         else:
             cap = count_nplets(n, ctx.lo, ctx.hi)
         cand, c = filt(1, cap)
+        if c < 0:
+            return False
         if c > cap:                                     # loose sample: exact size, once more
             cand, c = filt(1, c)
         # exact k best (+ ties at the k-th key) among the candidates

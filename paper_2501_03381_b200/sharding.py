@@ -1,9 +1,20 @@
-"""Multi-GPU sharding of the n-plet rank space (one process per GPU).
+"""Multi-GPU sharding of the n-plet space (one process per GPU).
 
-Every (n-plet, dataset) is independent, so the global order-major
-lexicographic rank space [0, total) is cut into contiguous ranges, one per
-rank, balanced by cost.  Nothing is exchanged while computing; the only
-collectives are the final merges:
+Every (n-plet, dataset) is independent, so nothing is exchanged while
+computing.  Two partitions:
+
+* lattice engine (12 <= N <= 32, power-of-two world): BLOCK shards -- rank
+  r owns the log-det table blocks whose top log2(world) prefix bits equal r
+  (ScanCtx.full_shard / hoi_lattice_shard).  It rebuilds only the table
+  chunks its stencil reads (its own and those with one of its bits
+  cleared: at most 1 + log2(world) of `world` chunks) and streams only its
+  own blocks, so both phases shrink with the world size; rank-range
+  shards would each stream nearly every block (a contiguous range of the
+  order-major order touches blocks of almost every prefix pattern).
+* otherwise: the global order-major lexicographic rank space [0, total)
+  cut into contiguous ranges, one per rank, balanced by cost.
+
+The only collectives are the final merges:
 
 * full output -- shards are contiguous slices of the global order, so
   concatenating them in rank order is bit-identical to a one-GPU scan;
@@ -89,16 +100,35 @@ def allreduce_counts(counts: np.ndarray, group=None, device="cpu") -> np.ndarray
     return t.cpu().numpy()
 
 
+def block_shard_bits(n: int, world: int):
+    """log2(world) when the lattice engine can block-shard N variables over
+    `world` ranks (power of two, at most (N-10)/2 shard bits), else None."""
+    sb = world.bit_length() - 1
+    if world < 1 or (1 << sb) != world or not 12 <= n <= 32 or sb > (n - 10) // 2:
+        return None
+    return sb
+
+
 def scan_sharded(covs, lo, hi, reducer, *, bias_correct=False, group=None):
-    """Run this rank's slice of an exhaustive scan on its GPU and merge the
+    """Run this rank's shard of an exhaustive scan on its GPU and merge the
     TopK / Histogram result across ranks (all ranks return the same value)."""
     import torch.distributed as dist
 
     from .nplet_engine import _raise_not_pd
-    from .scanner import Histogram, MEASURES, TopK, _ScanCtx, _topk_plane
+    from .scanner import Histogram, MEASURES, TopK, _ScanCtx, _topk_lattice, _topk_plane
     import torch
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = covs.n_variables
+    sb = block_shard_bits(n, world)
+    if type(reducer) is TopK and sb is not None:
+        ctx = _ScanCtx(covs, lo, hi, bias_correct)
+        ok = ctx.engine == 2 and _topk_lattice(ctx, reducer, MEASURES.index(reducer.measure),
+                                               shard=rank, shard_bits=sb)
+        if all(allgather_objects(bool(ok), group)):
+            parts = allgather_objects(reducer._best, group)
+            reducer._best = merge_topk(parts, reducer.k)
+            return reducer.finalize()
+        reducer._best = None                       # a rank declined: rank-range path
     weight = "count" if n <= 34 else "flops"
     g0, g1 = rank_ranges(n, lo, hi, world, weight)[rank]
     ctx = _ScanCtx(covs, lo, hi, bias_correct)

@@ -44,11 +44,39 @@ def test_rank_ranges_partition_the_space():
     assert max(costs) / min(costs) < 1.01
 
 
+def test_block_shards_partition_the_space():
+    """Lattice block shards (top shard_bits prefix variables) partition the
+    rank space into equal halves/quarters, and each shard's stencil only
+    reads table chunks equal to the shard with at most one bit cleared."""
+    from paper_2501_03381_b200.scanner import shard_rows
+    n, lo, hi = 14, 2, 14
+    total = sum(math.comb(n, k) for k in range(lo, hi + 1))
+    for sb in (1, 2):
+        parts = [shard_rows(n, lo, hi, r, sb) for r in range(1 << sb)]
+        allr = np.sort(np.concatenate(parts))
+        np.testing.assert_array_equal(allr, np.arange(total))
+        # a subset S of shard r: its leave-one-out neighbours S \ j lie in
+        # shard r (j outside the shard bits) or r with one bit cleared
+        lo_var = n - 10 - sb
+        for r in range(1 << sb):
+            need = {r} | {r & ~(1 << t) for t in range(sb) if (r >> t) & 1}
+            for c in itertools.islice(itertools.combinations(range(n), 6), 0, 3000, 7):
+                pat = sum(1 << (v - lo_var) for v in c if lo_var <= v < n - 10)
+                if pat != r:
+                    continue
+                for j in c:
+                    rest = [v for v in c if v != j]
+                    p2 = sum(1 << (v - lo_var) for v in rest if lo_var <= v < n - 10)
+                    assert p2 in need
+    assert sharding.block_shard_bits(30, 8) == 3 and sharding.block_shard_bits(30, 6) is None
+    assert sharding.block_shard_bits(12, 2) == 1 and sharding.block_shard_bits(11, 2) is None
+
+
 def _rows(n, lo, hi):
     return [c for k in range(lo, hi + 1) for c in itertools.combinations(range(n), k)]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode="ranges"):
     import sys
     from pathlib import Path
     repo = Path(__file__).resolve().parents[1]
@@ -63,8 +91,14 @@ def _worker(rank, world, port, q):
         a = rng.standard_normal((24, 8))
         sig = a.T @ a / 24 + 0.3 * np.eye(8)
         n, lo, hi, k = 8, 2, 8, 7
-        g0, g1 = sharding.rank_ranges(n, lo, hi, world, "count")[rank]
-        rows = _rows(n, lo, hi)[g0:g1]
+        if mode == "ranges":
+            g0, g1 = sharding.rank_ranges(n, lo, hi, world, "count")[rank]
+            rows = _rows(n, lo, hi)[g0:g1]
+        else:   # block-shard membership pattern (variables 1..2 of 8 for 2 bits; model only)
+            from paper_2501_03381_b200.scanner import shard_rows
+            allrows = _rows(14, lo, 14)
+            rows = [r for r in (allrows[i] for i in shard_rows(14, lo, 14, rank, 1))
+                    if max(r) < n and len(r) <= hi]
         best = []
         hist = np.zeros((1, 6), dtype=np.int64)
         edges = np.linspace(-0.2, 1.0, 7)
@@ -90,11 +124,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_rank_topk_and_histogram_merge(oracle):
+@pytest.mark.parametrize("mode", ["ranges", "blocks"])
+def test_two_rank_topk_and_histogram_merge(oracle, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
     got_top, got_counts = q.get(timeout=120)
