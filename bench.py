@@ -46,6 +46,7 @@ def args_():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-percell", action="store_true", help="skip the per-n-plet engine leg")
+    p.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 batched-evaluation leg")
     return p.parse_args()
 
 
@@ -319,6 +320,97 @@ def percell_roofline(torch, lib, nat, covs, g0, g1, step_ms):
     return r
 
 
+def cfg5_batched(a, torch, hoi, lib, nat, peak64):
+    """BASELINE config 5 (extra leg, not the headline): D=16 AR(1) datasets,
+    N=400, T=1200; 4,000,000 seeded order-10 n-plets evaluated on every
+    dataset (64M (n-plet, dataset) units) and the top-1,000 most negative
+    O-information n-plets per dataset.  Device timing of the fused
+    per-n-plet kernel and of kernel + per-dataset TopK select; e2e through
+    topk_batch from host index arrays; CPU oracle on a bounded sample."""
+    from paper_2501_03381_b200 import workloads
+    from paper_2501_03381_b200._device import device_covs
+    from paper_2501_03381_b200.scanner import MEASURES, _BatchCtx, _topk_plane
+    from paper_2501_03381_b200.sharding import nplet_flops
+    xs = [workloads.cfg5_data(d) for d in range(16)]
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x)) for x in xs])
+    idx = workloads.cfg5_nplets()
+    B, D, K = idx.shape[0], 16, 10
+    st = device_covs(covs)
+    didx = torch.from_numpy(idx.astype(np.int32)).cuda()
+    out = torch.empty((4, B, D), dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    coords = torch.zeros(128, dtype=torch.int64, device="cuda")
+    s = nat.stream_handle(torch)
+
+    def ev():
+        nat.check(lib.hoi_eval_indices(st.corr.data_ptr(), st.sdiag.data_ptr(), None, 0, 400, D,
+                                       didx.data_ptr(), B, K, out.data_ptr(), None, None,
+                                       cnt.data_ptr(), coords.data_ptr(), 64, s), "eval")
+
+    def ev_topk():
+        ev()
+        red = hoi.TopK("o", "min", 1000)
+        _topk_plane(_BatchCtx(D, torch), red, out, 0, 2,
+                    lambda pos: [tuple(r) for r in idx[np.asarray(pos)].tolist()])
+        return red
+
+    for _ in range(3):
+        ev_topk()
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    for _ in range(a.steps):
+        ev()
+    e[1].record()
+    torch.cuda.synchronize()
+    kms = e[0].elapsed_time(e[1]) / a.steps
+    t0 = time.perf_counter()
+    for _ in range(3):
+        ev_topk()
+    torch.cuda.synchronize()
+    step_s = (time.perf_counter() - t0) / 3
+    units = B * D
+    flops = units * nplet_flops(K)
+    # public API end to end: host index array -> device -> measures -> top-k on the host
+    batch = hoi.NpletBatch(400, indices=idx, check_unique=False)
+    times = []
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = hoi.topk_batch(covs, batch, hoi.TopK("o", "min", 1000)).finalize()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(times[1:]))
+    # CPU oracle (the reference's LAPACK route) on the first 20,000 n-plets
+    sys.path.insert(0, str(REPO / "oracle"))
+    import hoi_oracle as ora
+    sig = np.stack([c.sigma for c in covs.covs])
+    ns = 20000
+    t0 = time.perf_counter()
+    ora.hoi_batch(sig, [1200] * D, idx=idx[:ns])
+    cpu_s = time.perf_counter() - t0
+    return {
+        "workload": "cfg5: D=16 AR(1) datasets, N=400, T=1200; 4,000,000 order-10 n-plets x 16 "
+                    "datasets; TopK('o','min',1000) per dataset",
+        "unit": "n-plet*dataset/s",
+        "value": units / (step_s),
+        "kernel_only": units / (kms * 1e-3),
+        "kernel_ms": kms, "step_ms_with_topk": step_s * 1e3,
+        "e2e": {"value": units / e2e_s, "seconds_per_step": e2e_s,
+                "h2d_bytes_per_step": int(idx.size * 4 + sig.nbytes),
+                "d2h_bytes_per_step": int(len(res) * 1000 * (8 * 5 + 8 * K)),
+                "call": "topk_batch(covs, NpletBatch(400, indices=idx), TopK('o','min',1000))"},
+        "roofline": {"bound": "fp64 (gather-limited: 45 f64 of R per unit from L2)",
+                     "achieved": flops / (kms * 1e-3) / 1e12, "peak": peak64, "unit": "TFLOP/s",
+                     "frac": flops / (kms * 1e-3) / 1e12 / peak64,
+                     "flops_per_unit": nplet_flops(K), "gather_bytes_per_unit": 45 * 8,
+                     "hbm_out_bytes_per_unit": 32},
+        "cpu_baseline": {"value": ns * D / cpu_s, "unit": "n-plet*dataset/s", "cores": 1,
+                         "kind": "port", "sample": f"first {ns} n-plets x 16 datasets through the "
+                         f"oracle port (numpy/LAPACK, {cpu_s:.2f} s)"},
+    }
+
+
 def b200_arm(a):
     import torch
     world, rank, local = dist_env()
@@ -418,6 +510,12 @@ def b200_arm(a):
         # the headline numbers are final here; print them once early so a
         # later failure cannot lose them (the last line printed is the record)
         print(json.dumps(line), file=sys.stderr, flush=True)
+    if rank == 0 and world == 1 and not a.no_cfg5:
+        try:
+            peak64 = fp64["peak"] if fp64 else fp64_peak(torch, lib, nat)
+            line["cfg5_batched"] = cfg5_batched(a, torch, hoi, lib, nat, peak64)
+        except Exception as exc:  # reported, never silently dropped
+            line["cfg5_batched"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0 and not a.no_e2e:
         try:
             line["e2e"] = e2e(a, torch, hoi)

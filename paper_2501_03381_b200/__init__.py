@@ -63,6 +63,7 @@ from .scanner import (
     extract_features,
     scan,
     scan_device,
+    topk_batch,
 )
 from .synthetic import block_concat, ground_truth_hoi, r_system_cov, s_system_cov, sample_gaussian
 

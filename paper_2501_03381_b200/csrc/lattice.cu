@@ -56,6 +56,7 @@ __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
 // Global copies of the tables that are indexed per lane (constant memory
 // serialises divergent indices; these go through L1 with coalescing).
 __device__ uint16_t g_runmask[BLK];
+__device__ uint32_t g_run[BLK];          // run position p -> e | lexrank << 10 | q << 20
 __device__ uint64_t g_binom[kBinomN * kBinomN];
 
 __device__ __forceinline__ uint64_t binom_g(int n, int m) {
@@ -360,11 +361,14 @@ constexpr int PER = BLK / kStencilThreads;
 
 // Dynamic shared memory of the stencil kernel (kRing 8 KB table blocks in
 // flight per CTA).
-template <int kRing>
+// kNbs = 1: one neighbour-sum buffer (a second consumer barrier per block,
+// 12 KB less shared memory per CTA -> one more ring slot at 4 CTAs/SM; the
+// run table is then read from the global copy g_run through L1).
+template <int kRing, int kNbs = 2>
 struct StencilSmem {
-  double ring[kRing][BLK];           // TMA destination ring (48 KB)
-  double nbs[2][BLK];                // sum of the k leave-one-out log-dets per entry
-  uint32_t run[BLK];                 // run position p -> e | lexrank << 10 | q << 20
+  double ring[kRing][BLK];           // TMA destination ring
+  double nbs[kNbs][BLK];             // sum of the k leave-one-out log-dets per entry
+  uint32_t run[kNbs == 2 ? BLK : 1]; // run position p -> e | lexrank << 10 | q << 20
   uint64_t full[kRing];              // TMA landed
   uint64_t empty[kRing];             // every consumer warp is done with the slot
   int64_t base[2][CB + 1];           // output row of the first n-plet of run q
@@ -530,7 +534,7 @@ k_compact_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb,
 
 enum { MODE_FULL = 0, MODE_FILTER = 1, MODE_LOWSUM = 2 };
 
-template <int kRing, int kMinCtas, int MODE>
+template <int kRing, int kMinCtas, int MODE, int NB = 2>
 __global__ void __launch_bounds__(kStencilThreads + 32, kMinCtas)
 k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
@@ -541,11 +545,11 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   constexpr bool FILTER = MODE == MODE_FILTER;
   constexpr bool OWN = MODE != MODE_LOWSUM;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  StencilSmem<kRing> &sm = *reinterpret_cast<StencilSmem<kRing> *>(smem_raw);
+  StencilSmem<kRing, NB> &sm = *reinterpret_cast<StencilSmem<kRing, NB> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (OWN) {
+  if (OWN && NB == 2) {
     for (int p = tid; p < BLK; p += blockDim.x) {
       const int e = __ldg(g_runmask + p);
       const int q = __popc(e);
@@ -683,7 +687,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const int slot = J % kRing;
     mbar_wait(&sm.full[slot], (J / kRing) & 1u);
     const double *own = sm.ring[slot];
-    double *nbs = sm.nbs[buf];
+    double *nbs = sm.nbs[NB == 2 ? buf : 0];
 #pragma unroll
     for (int r = 0; r < PAIRS; ++r) {
       const int e0 = 2 * (tid + kStencilThreads * r);
@@ -706,7 +710,8 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     named_bar_sync(1, kStencilThreads);           // nbs[buf] and base[buf] complete
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-      const uint32_t w = sm.run[tid + kStencilThreads * r];
+      const uint32_t w = NB == 2 ? sm.run[tid + kStencilThreads * r]
+                                 : __ldg(g_run + tid + kStencilThreads * r);
       const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
       const int64_t b0 = sm.base[buf][q];
       const int k = kP + q;
@@ -762,6 +767,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);  // own slot free
+    if (NB == 1) named_bar_sync(1, kStencilThreads);   // nbs free for the next block
     ++J;
   }
 }
@@ -1021,6 +1027,14 @@ void upload_tables() {
   cudaMemcpyToSymbol(g_logtab, lt.data(), sizeof(double2) * 256);
   cudaMemcpyToSymbol(g_runmask, rm.data(), sizeof(uint16_t) * BLK);
   {
+    std::vector<uint32_t> gr(BLK);
+    for (int p = 0; p < BLK; ++p) {
+      const int e = rm[p], q = __builtin_popcount(e);
+      gr[p] = (uint32_t)e | ((uint32_t)(p - rs[q]) << 10) | ((uint32_t)q << 20);
+    }
+    cudaMemcpyToSymbol(g_run, gr.data(), sizeof(uint32_t) * BLK);
+  }
+  {
     std::vector<uint64_t> hb(kBinomN * kBinomN);
     fill_binomials(hb.data());
     cudaMemcpyToSymbol(g_binom, hb.data(), sizeof(uint64_t) * hb.size());
@@ -1158,7 +1172,7 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   return acc;
 }
 
-template <int R, int C, int F>
+template <int R, int C, int F, int NB = 2>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                        int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
@@ -1168,12 +1182,12 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
   static thread_local int grid_cap = 0, n_sms = 0, max_per_sm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int smem = (int)sizeof(StencilSmem<R>);
+  const int smem = (int)sizeof(StencilSmem<R, NB>);
   if (set_for != dev) {
-    cudaFuncSetAttribute(k_lattice_measures<R, C, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_lattice_measures<R, C, F, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C, F>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C, F, NB>,
                                                   kStencilThreads + 32, smem);
     max_per_sm = per_sm > 0 ? per_sm : 1;
     n_sms = sms;
@@ -1185,7 +1199,7 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
   if (per_sm_cap > 0 && per_sm_cap < max_per_sm) cap = (unsigned)(n_sms * per_sm_cap);
   const unsigned grid = n < cap ? n : cap;
   if (grid == 0) return HOI_OK;
-  k_lattice_measures<R, C, F><<<grid, kStencilThreads + 32, smem, s>>>(
+  k_lattice_measures<R, C, F, NB><<<grid, kStencilThreads + 32, smem, s>>>(
       w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
       blk_end, active, near_bits, w.counter, own_last, flt, ps);
   return check_launch("k_lattice_measures");
@@ -1252,18 +1266,30 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   if (two) {
     StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist};
     cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
-    int st = run_stencil<4, 4, MODE_LOWSUM>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
-                                            out, plane, blk_begin, blk_end, active, near_bits,
-                                            own_last, per_sm_cap, none, p1, s);
+    int st = ring == 5
+                 ? run_stencil<5, 4, MODE_LOWSUM, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
+                                                     g_end, out, plane, blk_begin, blk_end, active,
+                                                     near_bits, own_last, per_sm_cap, none, p1, s)
+                 : run_stencil<4, 4, MODE_LOWSUM>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
+                                                  g_end, out, plane, blk_begin, blk_end, active,
+                                                  near_bits, own_last, per_sm_cap, none, p1, s);
     if (st) return st;
     ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
                      listed ? cnts + 1 : nullptr};
   }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+  if (flt && ring == 5)
+    return run_stencil<5, 4, MODE_FILTER, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
+                                             g_end, out, plane, blk_begin, blk_end, active,
+                                             near_bits, own_last, per_sm_cap, *flt, ps, s);
   if (flt)
     return run_stencil<4, 4, MODE_FILTER>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
                                           out, plane, blk_begin, blk_end, active, near_bits,
                                           own_last, per_sm_cap, *flt, ps, s);
+  if (ring == 5)
+    return run_stencil<5, 4, MODE_FULL, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
+                                           out, plane, blk_begin, blk_end, active, near_bits,
+                                           own_last, per_sm_cap, none, ps, s);
   if (ring == 6)
     return run_stencil<6, 3, MODE_FULL>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
                                         plane, blk_begin, blk_end, active, near_bits, own_last,

@@ -76,11 +76,22 @@ k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double si
   __shared__ unsigned int h[kRadixBins];
   for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
+  int cur = -1;
+  unsigned run = 0;     // run-length aggregation (see k_radix_hist_multi)
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     uint64_t key = orderable_key(sign * vals[p * D + d]);
-    if ((key & hi_mask) == prefix) atomicAdd(&h[(key >> shift) & (kRadixBins - 1)], 1u);
+    if ((key & hi_mask) != prefix) continue;
+    const int b = (int)((key >> shift) & (kRadixBins - 1));
+    if (b == cur) {
+      ++run;
+    } else {
+      if (run) atomicAdd(&h[cur], run);
+      cur = b;
+      run = 1;
+    }
   }
+  if (run) atomicAdd(&h[cur], run);
   __syncthreads();
   for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x)
     if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
@@ -94,6 +105,71 @@ __global__ void k_key_filter(const double *__restrict__ vals, int64_t n, int D, 
     if (orderable_key(sign * vals[p * D + d]) <= key_max) {
       unsigned long long slot = atomicAdd(count, 1ull);
       if ((int64_t)slot < cap) cand[slot] = p;
+    }
+  }
+}
+
+// Multi-dataset radix select (all D datasets of a plane in lockstep):
+// 8-bit digits, per-dataset histograms in shared memory (D <= 64).
+constexpr int kMBits = 8;
+constexpr int kMBins = 1 << kMBits;
+
+// One dataset per lane slot (t % D), warp-private D x 256 histograms in
+// shared memory: lanes of a warp cover 32 consecutive (row, dataset)
+// elements, so at most ceil(32 / D)-way contention, none across warps.
+// Consecutive hits to the same bin are counted in a register first (the
+// leading digits put almost every value in a handful of bins).
+__global__ void k_radix_hist_multi(const double *__restrict__ vals, int64_t n, int D, double sign,
+                                   const uint64_t *__restrict__ prefix,
+                                   const uint64_t *__restrict__ hi_mask,
+                                   const int *__restrict__ live, int shift,
+                                   unsigned long long *__restrict__ counts) {
+  extern __shared__ unsigned int hm[];
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const int bins = D * kMBins;
+  for (int i = threadIdx.x; i < nw * bins; i += blockDim.x) hm[i] = 0;
+  __syncthreads();
+  unsigned int *my = hm + w * bins;
+  const int64_t total = n * D;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;     // a multiple of D
+  const int d = (int)(t0 % D);
+  if (live[d]) {
+    const uint64_t pre = prefix[d], msk = hi_mask[d];
+    int cur = -1;
+    unsigned run = 0;
+    for (int64_t t = t0; t < total; t += stride) {
+      const uint64_t key = orderable_key(sign * vals[t]);
+      if ((key & msk) != pre) continue;
+      const int b = (int)((key >> shift) & (kMBins - 1));
+      if (b == cur) {
+        ++run;
+      } else {
+        if (run) atomicAdd(&my[d * kMBins + cur], run);
+        cur = b;
+        run = 1;
+      }
+    }
+    if (run) atomicAdd(&my[d * kMBins + cur], run);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) {
+    unsigned v = 0;
+    for (int x = 0; x < nw; ++x) v += hm[x * bins + i];
+    if (v) atomicAdd(&counts[i], (unsigned long long)v);
+  }
+}
+
+__global__ void k_key_filter_multi(const double *__restrict__ vals, int64_t n, int D, double sign,
+                                   const uint64_t *__restrict__ key_max, int64_t *__restrict__ cand,
+                                   unsigned long long *__restrict__ count, int64_t cap) {
+  const int64_t total = n * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(t % D);
+    if (orderable_key(sign * vals[t]) <= key_max[d]) {
+      const unsigned long long slot = atomicAdd(&count[d], 1ull);
+      if ((int64_t)slot < cap) cand[(int64_t)d * cap + slot] = t / D;
     }
   }
 }
@@ -184,6 +260,80 @@ extern "C" int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t
   cudaMemcpyAsync(&c, ccount, sizeof(c), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   *h_count = (int64_t)c;
+  return HOI_OK;
+}
+
+// hoi_topk_select for every dataset of a (n, D) plane at once (D <= 64):
+// candidates of dataset d go to cand[d * cand_cap ...], their count to
+// h_counts[d] (HOST).  ws: device workspace of at least
+// D * 256 + 4 * D + 64 uint64.  Synchronous.
+extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign,
+                                     int64_t k, int64_t bucket_cap, int64_t *cand,
+                                     int64_t cand_cap, int64_t *h_counts, void *ws,
+                                     void *stream) {
+  HOI_CHECK_ARG(vals && cand && h_counts && ws && D >= 1 && D <= 64 && k >= 1 && n >= 0,
+                "hoi_topk_select_multi: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
+  uint64_t *d_prefix = reinterpret_cast<uint64_t *>(counts + (size_t)D * kMBins);
+  uint64_t *d_mask = d_prefix + D;
+  uint64_t *d_keymax = d_mask + D;
+  int *d_live = reinterpret_cast<int *>(d_keymax + D);
+  std::vector<unsigned long long> h((size_t)D * kMBins);
+  std::vector<uint64_t> prefix(D, 0), mask(D, 0), keymax(D, ~0ull);
+  std::vector<int64_t> need(D, k < n ? k : n);
+  std::vector<int> live(D, k < n ? 1 : 0);
+  // warps per block: D x 256 x 4 B of private histogram per warp, <= 64 KB
+  int nw = (64 * 1024) / (D * kMBins * 4);
+  nw = nw < 1 ? 1 : (nw > 8 ? 8 : nw);
+  int bs = 32 * nw;
+  bs = (bs / D) * D;                              // a multiple of D: one dataset per thread
+  if (bs < D) bs = D;
+  const size_t shm = sizeof(unsigned int) * D * kMBins * ((bs + 31) / 32);
+  const int blocks = 8 * sm_count();
+  cudaFuncSetAttribute(k_radix_hist_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+  for (int shift = 64 - kMBits; shift >= 0; shift -= kMBits) {
+    bool any = false;
+    for (int d = 0; d < D; ++d) any = any || live[d];
+    if (!any) break;
+    cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * D * kMBins, s);
+    cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_mask, mask.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_live, live.data(), sizeof(int) * D, cudaMemcpyHostToDevice, s);
+    k_radix_hist_multi<<<blocks, bs, shm, s>>>(vals, n, D, sign, d_prefix, d_mask, d_live, shift,
+                                               counts);
+    int st = check_launch("k_radix_hist_multi");
+    if (st) return st;
+    cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * D * kMBins,
+                    cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (int d = 0; d < D; ++d) {
+      if (!live[d]) continue;
+      int64_t acc = 0;
+      int b = 0;
+      const unsigned long long *hd = h.data() + (size_t)d * kMBins;
+      for (; b < kMBins; ++b) {
+        if (acc + (int64_t)hd[b] >= need[d]) break;
+        acc += (int64_t)hd[b];
+      }
+      need[d] -= acc;
+      prefix[d] |= (uint64_t)b << shift;
+      mask[d] |= (uint64_t)(kMBins - 1) << shift;
+      keymax[d] = prefix[d] | (shift ? ((1ull << shift) - 1) : 0ull);
+      if ((int64_t)hd[b] <= bucket_cap || shift == 0) live[d] = 0;
+    }
+  }
+  unsigned long long *ccount = reinterpret_cast<unsigned long long *>(d_live + 64);
+  cudaMemcpyAsync(d_keymax, keymax.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(ccount, 0, sizeof(unsigned long long) * D, s);
+  k_key_filter_multi<<<8 * sm_count(), 256, 0, s>>>(vals, n, D, sign, d_keymax, cand, ccount,
+                                                     cand_cap);
+  int st = check_launch("k_key_filter_multi");
+  if (st) return st;
+  std::vector<unsigned long long> c(D);
+  cudaMemcpyAsync(c.data(), ccount, sizeof(unsigned long long) * D, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  for (int d = 0; d < D; ++d) h_counts[d] = (int64_t)c[d];
   return HOI_OK;
 }
 

@@ -495,13 +495,14 @@ def _emit_progress(progress, n, lo, hi, batch_size, total, t0):
                   "elapsed": time.perf_counter() - t0})
 
 
-def _topk_plane(ctx, reducer, out, g0, m_idx):
+def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
     """Merge one device chunk into the running per-dataset TopK lists.
 
     The device radix-selects the k smallest keys sign*value (plus the rest
     of the k-th key's final radix bucket, so every tie is present); only
     those candidates reach the host, where the reference's exact key
-    (sign*value, index tuple) orders them."""
+    (sign*value, index tuple) orders them.  tuples_of(positions) gives the
+    index tuples of rows (default: device unranking of the scan ranks)."""
     torch = ctx.torch
     lib = nat.lib()
     rows = out.shape[1]
@@ -509,33 +510,79 @@ def _topk_plane(ctx, reducer, out, g0, m_idx):
     if reducer._best is None:
         reducer._best = [[] for _ in range(ctx.d)]
     plane = out[m_idx]
-    bucket_cap = max(4096, reducer.k)
-    cap = reducer.k + bucket_cap + 1
-    cand = torch.empty(cap, dtype=torch.int64, device="cuda")
-    ws = torch.empty(4096 + 64, dtype=torch.int64, device="cuda")
-    cnt = ctypes.c_int64(0)
+    # the multi-dataset select resolves 8 bits per pass, so it can narrow
+    # the k-th key's bucket to a few entries cheaply
+    bucket_cap = 64 if ctx.d > 1 else max(4096, reducer.k)
+    cap = reducer.k + max(bucket_cap, 4096) + 1
+    s = nat.stream_handle(torch)
+    if ctx.d > 1:
+        # every dataset of the plane in one multi-dataset radix select
+        cands = torch.empty((ctx.d, cap), dtype=torch.int64, device="cuda")
+        ws = torch.empty(ctx.d * 256 + 4 * ctx.d + 64, dtype=torch.int64, device="cuda")
+        hc = (ctypes.c_int64 * ctx.d)()
+        nat.check(lib.hoi_topk_select_multi(plane.data_ptr(), rows, ctx.d, sign, reducer.k,
+                                            bucket_cap, cands.data_ptr(), cap, hc,
+                                            ws.data_ptr(), s), "topk_select_multi")
+        counts = [int(hc[d]) for d in range(ctx.d)]
+    else:
+        cands = torch.empty((1, cap), dtype=torch.int64, device="cuda")
+        ws = torch.empty(4096 + 64, dtype=torch.int64, device="cuda")
+        cnt = ctypes.c_int64(0)
+        nat.check(lib.hoi_topk_select(plane.data_ptr(), rows, 1, 0, sign, reducer.k, bucket_cap,
+                                      cands.data_ptr(), cap, ctypes.byref(cnt), ws.data_ptr(), s),
+                  "topk_select")
+        counts = [int(cnt.value)]
     for d in range(ctx.d):
-        nat.check(lib.hoi_topk_select(plane.data_ptr(), rows, ctx.d, d, sign, reducer.k,
-                                      bucket_cap, cand.data_ptr(), cap, ctypes.byref(cnt),
-                                      ws.data_ptr(), nat.stream_handle(torch)), "topk_select")
-        c = int(cnt.value)
+        c = counts[d]
         if c > cap:
             # a tie wider than the candidate buffer at the k-th value (e.g.
             # identical covariances): resolve it with the reference's host
             # rule over the chunk, slice by slice
-            _topk_host_slices(ctx, reducer, out, g0, d)
+            if tuples_of is None:
+                _topk_host_slices(ctx, reducer, out, g0, d)
+            else:
+                _topk_host_rows(reducer, out, d, tuples_of)
             continue
-        pos = cand[:c]
+        pos = cands[d, :c]
         vals = out[:, pos, d].cpu().numpy()            # (4, c)
-        tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, (pos + g0).cpu().numpy()) if c else []
-        mv = vals[m_idx]
+        if c > reducer.k:
+            # keep the k best keys and every tie at the k-th before building
+            # Python objects (the exact tuple tie-break happens in _merge)
+            key = sign * vals[m_idx]
+            keep = np.flatnonzero(key <= np.partition(key, reducer.k - 1)[reducer.k - 1])
+            vals = vals[:, keep]
+            pos = pos[torch.from_numpy(keep).to(pos.device)]
+            c = keep.size
+        if tuples_of is not None:
+            tuples = tuples_of(pos.cpu().numpy())
+        else:
+            tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, (pos + g0).cpu().numpy()) if c else []
         new = []
-        for i in range(c):
-            e = TopEntry(indices=tuples[i], order=len(tuples[i]), value=float(mv[i]),
-                         tc=float(vals[0, i]), dtc=float(vals[1, i]), o=float(vals[2, i]),
-                         s=float(vals[3, i]))
-            new.append(((sign * e.value, e.indices), e))
+        for t, (tc, dtc, o, sv) in zip(tuples, vals.T.tolist()):
+            v = (tc, dtc, o, sv)[m_idx]
+            new.append(((sign * v, t), TopEntry(t, len(t), v, tc, dtc, o, sv)))
         reducer._merge(d, new)
+
+
+def _topk_host_rows(reducer, out, d, tuples_of):
+    """The reference's host TopK rule over one dataset of a device batch."""
+    v = out[:, :, d].cpu().numpy()
+    rows = v.shape[1]
+    sub = TopK(reducer.measure, reducer.direction, reducer.k)
+    sign = reducer.sign
+    key = sign * v[MEASURES.index(reducer.measure)]
+    k_eff = min(reducer.k, rows)
+    thr = np.partition(key, k_eff - 1)[k_eff - 1]
+    sel = np.flatnonzero(key <= thr)
+    tuples = tuples_of(sel)
+    new = []
+    for i, t in zip(sel, tuples):
+        e = TopEntry(indices=t, order=len(t), value=float(v[MEASURES.index(reducer.measure), i]),
+                     tc=float(v[0, i]), dtc=float(v[1, i]), o=float(v[2, i]), s=float(v[3, i]))
+        new.append(((sign * e.value, t), e))
+    sub._best = [[]]
+    sub._merge(0, new)
+    reducer._merge(d, sub._best[0])
 
 
 def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
@@ -652,6 +699,36 @@ def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
         reducer._merge(d, best[d])
     ctx._table_ok = ctx.d == 1
     return True
+
+
+class _BatchCtx:
+    """The fields _topk_plane reads, for a user batch on the device."""
+
+    def __init__(self, d, torch):
+        self.d, self.torch = d, torch
+
+
+def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: bool = False):
+    """``reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct))``
+    with the selection on the device (ref:scanner.py:75-100 semantics):
+    the four measures of the batch stay in HBM, a radix select per dataset
+    keeps the k best keys plus every tie, and only those rows reach the
+    reference's host merge (sign*value, index tuple).  Extension of the
+    reference API for large user batches (the greedy/anneal candidate
+    evaluations and BASELINE config 5: 4M order-10 n-plets x 16 datasets)."""
+    if not isinstance(reducer, TopK):
+        raise InvalidData("topk_batch needs a TopK reducer")
+    from .nplet_engine import eval_device
+    out, _, _ = eval_device(covs, batch, bias_correct, measures=True, terms=False)
+    ctx = _BatchCtx(out.shape[2], nat.torch_cuda())
+
+    def tuples_of(pos):
+        if batch.mode == "fixed":
+            return [tuple(r) for r in batch.indices[np.asarray(pos, dtype=np.int64)].tolist()]
+        return [batch.row_indices(int(i)) for i in pos]
+
+    _topk_plane(ctx, reducer, out, 0, MEASURES.index(reducer.measure), tuples_of)
+    return reducer
 
 
 def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):

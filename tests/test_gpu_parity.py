@@ -472,3 +472,20 @@ def test_block_shards_reassemble_the_scan(shard_bits):
     merged = sharding.merge_topk(parts, 500)
     single = hoi.scan(covs, 2, 24, hoi.TopK("o", "min", 500))[0]
     assert [e.indices for _, e in merged[0]] == [e.indices for e in single]
+
+
+def test_topk_batch_matches_host_reducer():
+    """Device batched TopK == the reference's TopK.update on the same
+    HoiBatch (cfg5-style: 16 datasets, N = 400, order-10 random n-plets)."""
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(d)))
+                       for d in range(16)])
+    idx = workloads.cfg5_nplets(b=30000)
+    batch = hoi.NpletBatch(400, indices=idx)
+    for measure, direction, k in [("o", "min", 100), ("s", "max", 7)]:
+        got = hoi.topk_batch(covs, batch, hoi.TopK(measure, direction, k)).finalize()
+        ref = hoi.TopK(measure, direction, k)
+        ref.update(batch, hoi.compute_hoi_batch(covs, batch))
+        want = ref.finalize()
+        for g, w in zip(got, want):
+            assert [e.indices for e in g] == [e.indices for e in w]
+            assert [(e.tc, e.dtc, e.o, e.s) for e in g] == [(e.tc, e.dtc, e.o, e.s) for e in w]
