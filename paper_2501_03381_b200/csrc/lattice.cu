@@ -346,6 +346,9 @@ __device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
                                             uint64_t *bar, uint64_t policy) {
   asm volatile(
@@ -497,6 +500,7 @@ struct StencilPass {
   int perm_lb;
   const unsigned *list;
   const unsigned *nlist;
+  int prefetch;       // claim-ahead L2 prefetch of the own / pass-1-sum blocks
 };
 
 // Compact the flagged blocks into a list in claim order (natural, or
@@ -566,6 +570,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   __syncthreads();
   const unsigned nbmask = ps.nbmask;
   const int nP = N - CB;
+  const bool pf_own = ps.prefetch != 0;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------ producer ----
@@ -573,23 +578,41 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const uint64_t pol_near = l2_policy(false), pol_far = l2_policy(true);
     const uint64_t pol_own = own_last ? l2_policy_last() : pol_near;
     const int hb = nP - ps.perm_lb;
-    uint32_t pJ = 0;
-    for (uint32_t seq = 0;; ++seq) {
-      unsigned P = kEndBlock;
+    auto claim = [&]() -> unsigned {
       if (ps.list) {
         const unsigned c = atomicAdd(counter, 1u);
-        if (c < *ps.nlist) P = ps.list[c];
-      } else {
-        for (;;) {
-          const unsigned c = atomicAdd(counter, 1u);
-          if (c >= blk_end - blk_begin) break;
-          const unsigned q = ps.perm_lb ? (((c & ((1u << hb) - 1u)) << ps.perm_lb) | (c >> hb)) : c;
-          if (!active || active[blk_begin + q]) {
-            P = blk_begin + q;
-            break;
-          }
-        }
+        return c < *ps.nlist ? ps.list[c] : kEndBlock;
       }
+      for (;;) {
+        const unsigned c = atomicAdd(counter, 1u);
+        if (c >= blk_end - blk_begin) return kEndBlock;
+        const unsigned q = ps.perm_lb ? (((c & ((1u << hb) - 1u)) << ps.perm_lb) | (c >> hb)) : c;
+        if (!active || active[blk_begin + q]) return blk_begin + q;
+      }
+    };
+    // Claim-ahead queue: blocks are claimed kLook ahead of streaming and
+    // their DRAM-sourced 8 KB blocks (own T[P], and the pass-1 sums) are
+    // prefetched into L2 at claim time, so the in-order TMA ring only ever
+    // waits for L2 hits.
+    constexpr int kLook = 4;
+    unsigned look[kLook];
+    auto prefetch = [&](unsigned Q) {
+      if (Q == kEndBlock || !pf_own) return;
+      if (OWN) l2_prefetch(table + (int64_t)Q * BLK, kBlkBytes);
+      if (ps.extra) l2_prefetch(ps.extra + (int64_t)Q * BLK, kBlkBytes);
+    };
+#pragma unroll
+    for (int i = 0; i < kLook; ++i) {
+      look[i] = claim();
+      prefetch(look[i]);
+    }
+    uint32_t pJ = 0;
+    for (uint32_t seq = 0;; ++seq) {
+      const unsigned P = look[0];
+#pragma unroll
+      for (int i = 0; i + 1 < kLook; ++i) look[i] = look[i + 1];
+      look[kLook - 1] = P == kEndBlock ? kEndBlock : claim();
+      prefetch(look[kLook - 1]);
       unsigned prem = P == kEndBlock ? 0u : (P & nbmask);
       // jobs of P: neighbours (far bits first), the partial-sum block, the own block
       int stage = prem ? 0 : (ps.extra ? 1 : (OWN ? 2 : 3));
@@ -1249,7 +1272,10 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
                    blk_end == (1u << nP) && w.lowsum;
   const int lb = nP / 2;
   const StencilFilter none{};
-  StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr};
+  // claim-ahead L2 prefetch of the own / pass-1-sum blocks: measured no
+  // gain on B200 (cfg4 19.75-19.89 ms with vs 19.16 without), off
+  static const int pf = getenv("HOI_PREFETCH") ? atoi(getenv("HOI_PREFETCH")) : 0;
+  StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr, pf};
   // partial / sampled scans over the whole block space: compacted block
   // lists (natural order for a single pass or pass 1, high-bits-fastest for
   // pass 2) in the workspace after the flags
@@ -1264,7 +1290,7 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     ps.nlist = cnts;
   }
   if (two) {
-    StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist};
+    StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0};
     cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
     int st = ring == 5
                  ? run_stencil<5, 4, MODE_LOWSUM, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
@@ -1275,7 +1301,7 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
                                                   near_bits, own_last, per_sm_cap, none, p1, s);
     if (st) return st;
     ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
-                     listed ? cnts + 1 : nullptr};
+                     listed ? cnts + 1 : nullptr, pf};
   }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
   if (flt && ring == 5)
