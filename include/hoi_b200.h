@@ -262,6 +262,15 @@ int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d,
                     double sign, const double *thresh, int64_t *cand,
                     int64_t *cand_count, int64_t cand_cap, void *stream);
 
+/* Optimiser objective (ref:optimizers.py:74-102): energy[b] = sign *
+ * aggregate of row b of a (B, D) plane over the D datasets -- mode 0 the
+ * mean, mode 1 the paired Cohen's d mean(v_a - v_b) / std(v_a - v_b, ddof 1)
+ * over the npairs (cond_a[i], cond_b[i]) (device int32 arrays).  A zero or
+ * non-finite pair deviation sets *degenerate (device int32, caller zeroes). */
+int hoi_objective(const double *vals, int64_t B, int32_t D, int32_t mode, const int32_t *cond_a,
+                  const int32_t *cond_b, int32_t npairs, double sign, double *energy,
+                  int32_t *degenerate, void *stream);
+
 /* Histogram with numpy.histogram semantics after clipping to [lo, hi]
  * (ref:scanner.py:126-134): counts (D, bins) int64 accumulated. */
 int hoi_histogram(const double *vals, int64_t n, int32_t D, int32_t bins,

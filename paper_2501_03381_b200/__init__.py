@@ -65,6 +65,24 @@ from .scanner import (
     scan_device,
     topk_batch,
 )
-from .synthetic import block_concat, ground_truth_hoi, r_system_cov, s_system_cov, sample_gaussian
+from .optimizers import (
+    AnnealSchedule,
+    GreedyResult,
+    ObjectiveSpec,
+    OptimState,
+    OrderBest,
+    anneal,
+    evaluate_objective,
+    greedy,
+)
+from .synthetic import (
+    PgmBlock,
+    PgmSpec,
+    block_concat,
+    ground_truth_hoi,
+    r_system_cov,
+    s_system_cov,
+    sample_gaussian,
+)
 
 __version__ = "0.1.0"

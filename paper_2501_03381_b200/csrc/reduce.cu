@@ -174,6 +174,39 @@ __global__ void k_key_filter_multi(const double *__restrict__ vals, int64_t n, i
   }
 }
 
+// Optimiser objective per row of a (B, D) plane (ref:optimizers.py:74-102):
+// mode 0: mean over the D datasets; mode 1: paired Cohen's d over the pairs
+// (cond_a[i], cond_b[i]): mean(diff) / std(diff, ddof=1).  energy = sign *
+// aggregate (sign -1 for direction 'min').  A zero or non-finite pair
+// standard deviation sets *degenerate.
+__global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, int mode,
+                            const int *__restrict__ ca, const int *__restrict__ cb, int np,
+                            double sign, double *__restrict__ energy, int *__restrict__ degenerate) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const double *row = vals + b * D;
+    double agg;
+    if (mode == 0) {
+      double acc = 0.0;
+      for (int d = 0; d < D; ++d) acc += row[d];
+      agg = acc / (double)D;
+    } else {
+      double mean = 0.0;
+      for (int i = 0; i < np; ++i) mean += row[ca[i]] - row[cb[i]];
+      mean /= (double)np;
+      double ss = 0.0;
+      for (int i = 0; i < np; ++i) {
+        const double x = (row[ca[i]] - row[cb[i]]) - mean;
+        ss += x * x;
+      }
+      const double sd = sqrt(ss / (double)(np - 1));
+      if (!(sd > 0.0) || !isfinite(sd)) atomicExch(degenerate, 1);
+      agg = mean / sd;
+    }
+    energy[b] = sign * agg;
+  }
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -378,6 +411,19 @@ extern "C" int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int3
   cudaMemcpyAsync(key_out, &key, sizeof(key), cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
   return HOI_OK;
+}
+
+extern "C" int hoi_objective(const double *vals, int64_t B, int32_t D, int32_t mode,
+                             const int32_t *cond_a, const int32_t *cond_b, int32_t npairs,
+                             double sign, double *energy, int32_t *degenerate, void *stream) {
+  HOI_CHECK_ARG(vals && energy && degenerate && B >= 0 && D >= 1 && (mode == 0 || mode == 1),
+                "hoi_objective: bad args");
+  HOI_CHECK_ARG(mode == 0 || (cond_a && cond_b && npairs >= 2), "hoi_objective: bad pairs");
+  if (B == 0) return HOI_OK;
+  const int64_t g = (B + 255) / 256;
+  k_objective<<<(int)(g < 8 * sm_count() ? g : 8 * sm_count()), 256, 0, (cudaStream_t)stream>>>(
+      vals, B, D, mode, cond_a, cond_b, npairs, sign, energy, degenerate);
+  return check_launch("k_objective");
 }
 
 extern "C" int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
