@@ -271,6 +271,16 @@ int hoi_objective(const double *vals, int64_t B, int32_t D, int32_t mode, const 
                   const int32_t *cond_b, int32_t npairs, double sign, double *energy,
                   int32_t *degenerate, void *stream);
 
+/* 21-feature accumulator partials (ref:scanner.py:205-287) of one
+ * full-output chunk: 4 planes of (rows, D) at global ranks g0 .. g0+rows-1;
+ * ranks in [pair_begin, pair_end) are the order-2 rows.  feat (device,
+ * D x 19 doubles): pair count, pair sum tc, pair sum tc^2, count (order >=
+ * 3), sums (tc dtc o s), maxima, minima, first global rank attaining the o
+ * maximum / minimum, count o < 0.  Deterministic (fixed reduction order).
+ * ws: device workspace of >= 8 * 148 * 256 * 19 doubles (ws_doubles). */
+int hoi_features(const double *out, int64_t rows, int32_t D, int64_t g0, int64_t pair_begin,
+                 int64_t pair_end, double *feat, void *ws, int64_t ws_doubles, void *stream);
+
 /* Histogram with numpy.histogram semantics after clipping to [lo, hi]
  * (ref:scanner.py:126-134): counts (D, bins) int64 accumulated. */
 int hoi_histogram(const double *vals, int64_t n, int32_t D, int32_t bins,

@@ -60,6 +60,7 @@ _SIGS = {
                          _vp, _vp], C.c_int),
     "hoi_topk_select_multi": ([_vp, _i64, _i32, _dbl, _i64, _i64, _vp, _i64, C.POINTER(_i64),
                                _vp, _vp], C.c_int),
+    "hoi_features": ([_vp, _i64, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_objective": ([_vp, _i64, _i32, _i32, _vp, _vp, _i32, _dbl, _vp, _vp, _vp], C.c_int),
     "hoi_topk_threshold": ([_vp, _i64, _i32, _i32, _dbl, _i64, _vp, _vp, _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),

@@ -207,6 +207,90 @@ __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, i
   }
 }
 
+// 21-feature accumulator (ref:scanner.py:205-287), device part.  Pass 1:
+// thread t (grid stride a multiple of D, so one dataset per thread) walks
+// its rows in increasing rank order and keeps partials; pass 2: one
+// thread per dataset reduces the partials of that dataset in thread order
+// (deterministic).  Fields per thread / per dataset:
+//  0 pair count, 1 sum tc (pairs), 2 sum tc^2 (pairs), 3 count (order >= 3),
+//  4..7 sum tc dtc o s, 8..11 max, 12..15 min, 16 first rank of the o max,
+//  17 first rank of the o min, 18 count o < 0.
+constexpr int kFeat = 19;
+
+__global__ void k_features_partial(const double *__restrict__ out, int64_t rows, int D,
+                                   int64_t plane, int64_t g0, int64_t pair_begin,
+                                   int64_t pair_end, double *__restrict__ part) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double f[kFeat];
+  for (int i = 0; i < kFeat; ++i) f[i] = 0.0;
+  for (int m = 0; m < 4; ++m) {
+    f[8 + m] = -INFINITY;
+    f[12 + m] = INFINITY;
+  }
+  f[16] = f[17] = -1.0;
+  const int64_t total = rows * D;
+  for (int64_t t = t0; t < total; t += stride) {
+    const int64_t r = t / D;
+    const int64_t g = g0 + r;
+    const double tc = out[t], dtc = out[plane + t], o = out[2 * plane + t], sv = out[3 * plane + t];
+    if (g >= pair_begin && g < pair_end) {
+      f[0] += 1.0;
+      f[1] += tc;
+      f[2] += tc * tc;
+      continue;
+    }
+    const double v[4] = {tc, dtc, o, sv};
+    f[3] += 1.0;
+    for (int m = 0; m < 4; ++m) {
+      f[4 + m] += v[m];
+      if (v[m] > f[8 + m]) {
+        f[8 + m] = v[m];
+        if (m == 2) f[16] = (double)g;
+      }
+      if (v[m] < f[12 + m]) {
+        f[12 + m] = v[m];
+        if (m == 2) f[17] = (double)g;
+      }
+    }
+    if (o < 0.0) f[18] += 1.0;
+  }
+  double *p = part + t0 * kFeat;
+  for (int i = 0; i < kFeat; ++i) p[i] = f[i];
+}
+
+__global__ void k_features_reduce(const double *__restrict__ part, int64_t nthreads, int D,
+                                  double *__restrict__ feat) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  double f[kFeat];
+  for (int i = 0; i < kFeat; ++i) f[i] = 0.0;
+  for (int m = 0; m < 4; ++m) {
+    f[8 + m] = -INFINITY;
+    f[12 + m] = INFINITY;
+  }
+  f[16] = f[17] = -1.0;
+  for (int64_t t = d; t < nthreads; t += D) {
+    const double *p = part + t * kFeat;
+    for (int i = 0; i < 8; ++i) f[i] += p[i];
+    for (int m = 0; m < 4; ++m) {
+      // max: larger wins, equal values keep the smaller first-attainment rank
+      if (p[8 + m] > f[8 + m] ||
+          (m == 2 && p[8 + m] == f[8 + m] && p[16] >= 0 && (f[16] < 0 || p[16] < f[16]))) {
+        f[8 + m] = p[8 + m];
+        if (m == 2) f[16] = p[16];
+      }
+      if (p[12 + m] < f[12 + m] ||
+          (m == 2 && p[12 + m] == f[12 + m] && p[17] >= 0 && (f[17] < 0 || p[17] < f[17]))) {
+        f[12 + m] = p[12 + m];
+        if (m == 2) f[17] = p[17];
+      }
+    }
+    f[18] += p[18];
+  }
+  for (int i = 0; i < kFeat; ++i) feat[(int64_t)d * kFeat + i] = f[i];
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -424,6 +508,29 @@ extern "C" int hoi_objective(const double *vals, int64_t B, int32_t D, int32_t m
   k_objective<<<(int)(g < 8 * sm_count() ? g : 8 * sm_count()), 256, 0, (cudaStream_t)stream>>>(
       vals, B, D, mode, cond_a, cond_b, npairs, sign, energy, degenerate);
   return check_launch("k_objective");
+}
+
+// Feature partials of a full-output chunk (4 planes of (rows, D), global
+// rank of row 0 = g0; rows with global rank in [pair_begin, pair_end) are
+// the order-2 pairs): feat (D, 19) doubles, see k_features_partial.
+// ws: device workspace of >= 8 * 148 * 256 * 19 doubles.
+extern "C" int hoi_features(const double *out, int64_t rows, int32_t D, int64_t g0,
+                            int64_t pair_begin, int64_t pair_end, double *feat, void *ws,
+                            int64_t ws_doubles, void *stream) {
+  HOI_CHECK_ARG(out && feat && ws && D >= 1 && rows >= 0, "hoi_features: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  int bs = (256 / D) * D;                      // a multiple of D: one dataset per thread
+  if (bs < D) bs = D;
+  int blocks = 4 * sm_count();
+  if ((int64_t)blocks * bs * kFeat > ws_doubles) blocks = (int)(ws_doubles / ((int64_t)bs * kFeat));
+  if (blocks < 1) return fail(HOI_CAPACITY, "hoi_features: workspace too small");
+  const int64_t nthreads = (int64_t)blocks * bs;
+  k_features_partial<<<blocks, bs, 0, s>>>(out, rows, D, rows * (int64_t)D, g0, pair_begin,
+                                           pair_end, reinterpret_cast<double *>(ws));
+  int st = check_launch("k_features_partial");
+  if (st) return st;
+  k_features_reduce<<<(D + 63) / 64, 64, 0, s>>>(reinterpret_cast<double *>(ws), nthreads, D, feat);
+  return check_launch("k_features_reduce");
 }
 
 extern "C" int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t d, double sign,

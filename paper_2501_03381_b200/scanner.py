@@ -731,6 +731,63 @@ def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: 
     return reducer
 
 
+def _scan_device_features(ctx, reducer, batch_size, progress, total, t0):
+    """FeatureAccumulator over device full-output chunks: hoi_features
+    reduces each chunk to 19 partials per dataset on the device (sums,
+    extrema with the first global rank attaining the o extremes, counts);
+    the host merges chunks in enumeration order into the accumulator's own
+    state, so finalize() is the reference's (ref:scanner.py:231-287)."""
+    torch, lib = ctx.torch, nat.lib()
+    n, d_count = ctx.n, ctx.d
+    if reducer._d is None:
+        reducer._init_state(d_count)
+    offs, acc = [], 0
+    for k in range(ctx.lo, ctx.hi + 1):
+        offs.append(acc)
+        acc += math.comb(n, k)
+    offs_np = np.asarray(offs, dtype=np.int64)
+    pb = pe = 0
+    if ctx.lo <= 2 <= ctx.hi:
+        pb = offs[2 - ctx.lo]
+        pe = pb + math.comb(n, 2)
+    whole_rank = offs[n - ctx.lo] if ctx.lo <= n <= ctx.hi else -1
+
+    def order_of(rank):
+        return ctx.lo + int(np.searchsorted(offs_np, rank, side="right")) - 1
+
+    feat = torch.empty((d_count, 19), dtype=torch.float64, device="cuda")
+    ws_doubles = 8 * 148 * 256 * 19
+    ws = torch.empty(ws_doubles, dtype=torch.float64, device="cuda")
+    per_chunk = _chunk_rows(d_count, torch)
+    g0 = 0
+    while g0 < total:
+        g1 = min(total, g0 + per_chunk)
+        out, cnt, coords = ctx.full(g0, g1, reuse_table=g0 > 0)
+        _raise_not_pd(cnt, coords)
+        nat.check(lib.hoi_features(out.data_ptr(), g1 - g0, d_count, g0, pb, pe, feat.data_ptr(),
+                                   ws.data_ptr(), ws_doubles, nat.stream_handle(torch)), "features")
+        f = feat.cpu().numpy()
+        reducer._mi_count += int(f[0, 0])
+        reducer._mi_sum += f[:, 1]
+        reducer._mi_sumsq += f[:, 2]
+        reducer._count += int(f[0, 3])
+        reducer._sums += f[:, 4:8]
+        reducer._syn += f[:, 18].astype(np.int64)
+        for d in range(d_count):
+            if f[d, 3] == 0:
+                continue
+            if f[d, 10] > reducer._maxs[d, 2]:
+                reducer._o_max_order[d] = order_of(int(f[d, 16]))
+            if f[d, 14] < reducer._mins[d, 2]:
+                reducer._o_min_order[d] = order_of(int(f[d, 17]))
+        np.maximum(reducer._maxs, f[:, 8:12], out=reducer._maxs)
+        np.minimum(reducer._mins, f[:, 12:16], out=reducer._mins)
+        if g0 <= whole_rank < g1:
+            reducer._whole = out[:, whole_rank - g0, :].cpu().numpy().T.copy()
+        g0 = g1
+    _emit_progress(progress, n, ctx.lo, ctx.hi, batch_size, total, t0)
+
+
 def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):
     torch = ctx.torch
     if isinstance(reducer, TopK) and ctx.engine == 2 and _topk_lattice(
@@ -799,6 +856,8 @@ def scan(covs: CovSet, min_order: int, max_order: int, reducer: Reducer, *,
     ctx = _ScanCtx(covs, min_order, max_order, bias_correct)
     if type(reducer) in (TopK, Histogram):
         _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0)
+    elif type(reducer) is FeatureAccumulator and reducer.n == n:
+        _scan_device_features(ctx, reducer, batch_size, progress, total, t0)
     else:
         _scan_stream(ctx, covs, reducer, batch_size, progress, total, t0)
     return reducer.finalize()

@@ -489,3 +489,23 @@ def test_topk_batch_matches_host_reducer():
         for g, w in zip(got, want):
             assert [e.indices for e in g] == [e.indices for e in w]
             assert [(e.tc, e.dtc, e.o, e.s) for e in g] == [(e.tc, e.dtc, e.o, e.s) for e in w]
+
+
+def test_device_features_match_host_replay():
+    """The device feature reducer equals the reference accumulator fed the
+    same device measures batch by batch (host replay, the generic Reducer
+    path), on 3 datasets of N = 16 over orders 2..16 and a sub-range."""
+    from paper_2501_03381_b200 import scanner
+    rng = np.random.default_rng(21)
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(
+        rng.standard_normal((600, 16)) @ np.linalg.cholesky(workloads.randcorr(16, rng)).T))
+        for _ in range(3)])
+    got = hoi.extract_features(covs)
+
+    class Replay(hoi.FeatureAccumulator):
+        pass                                   # not the exact type: takes the replay path
+
+    want = hoi.scan(covs, 2, 16, Replay(16), batch_size=3000)
+    for g, w in zip(got, want):
+        for name in hoi.FEATURE_NAMES:
+            assert getattr(g, name) == pytest.approx(getattr(w, name), rel=1e-11, abs=1e-12), name
