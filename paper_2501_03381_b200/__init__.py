@@ -62,6 +62,7 @@ from .scanner import (
     TopK,
     extract_features,
     scan,
+    read_scan,
     scan_device,
     topk_batch,
 )

@@ -288,6 +288,35 @@ class DeviceScan:
             acc += math.comb(self.n, k)
         return off
 
+    def save(self, path, chunk_rows: int = 1 << 24):
+        """Write the scan in the binary scan format (the
+        full output of an exhaustive scan -- 34 GB for N = 30 -- has no CSV
+        form): a 4096-byte JSON header (format, n, orders, rank range, D,
+        plane order, dtype), then the four float64 planes tc, dtc, o, s,
+        each (rows, D) in global rank order, rank implicit (row i is rank
+        g_begin + i; `unrank` maps it to its index tuple).  Streamed from HBM
+        in chunks through a pinned staging buffer.  read_scan() maps it back."""
+        import json
+        torch = nat.torch_cuda()
+        rows, d = self.out.shape[1], self.out.shape[2]
+        head = json.dumps({"format": "hoi-b200-scan/1", "n": self.n, "min_order": self.min_order,
+                           "max_order": self.max_order, "g_begin": self.g_begin,
+                           "g_end": self.g_end, "datasets": d, "planes": list(MEASURES),
+                           "dtype": "float64", "layout": "planes x rows x datasets, C order",
+                           "header_bytes": 4096}).encode()
+        if len(head) > 4096:
+            raise InvalidData("scan header too long")
+        step = max(1, min(chunk_rows, rows))
+        stage = torch.empty((step, d), dtype=torch.float64, pin_memory=True)
+        with open(path, "wb") as f:
+            f.write(head.ljust(4096, b" "))
+            for q in range(4):
+                for a in range(0, rows, step):
+                    b = min(rows, a + step)
+                    stage[:b - a].copy_(self.out[q, a:b])
+                    f.write(stage[:b - a].numpy().tobytes())
+        return path
+
 
 class _ScanCtx:
     def __init__(self, covs, lo, hi, bias_correct, engine=0):
@@ -392,6 +421,20 @@ def shard_rows(n: int, lo: int, hi: int, shard: int, shard_bits: int) -> np.ndar
                 rows.append(g)
             g += 1
     return np.asarray(rows, dtype=np.int64)
+
+
+def read_scan(path):
+    """(header dict, (4, rows, D) float64 memmap) of a file written by
+    DeviceScan.save (host only; no device needed)."""
+    import json
+    with open(path, "rb") as f:
+        head = json.loads(f.read(4096).decode())
+    if head.get("format") != "hoi-b200-scan/1":
+        raise InvalidData(f"{path}: not a hoi-b200 scan file")
+    rows = head["g_end"] - head["g_begin"]
+    planes = np.memmap(path, dtype=np.float64, mode="r", offset=head["header_bytes"],
+                       shape=(4, rows, head["datasets"]))
+    return head, planes
 
 
 def scan_device(covs: CovSet, min_order: int, max_order: int, *, bias_correct: bool = False,

@@ -509,3 +509,16 @@ def test_device_features_match_host_replay():
     for g, w in zip(got, want):
         for name in hoi.FEATURE_NAMES:
             assert getattr(g, name) == pytest.approx(getattr(w, name), rel=1e-11, abs=1e-12), name
+
+
+def test_scan_file_round_trip(tmp_path, golden):
+    """Binary scan format: cfg1's device output written in small chunks and
+    read back through the host memmap reader equals the golden values."""
+    g = golden.npz("cfg1")
+    covs = hoi.CovSet([hoi.CovarianceMatrix(g["cov"])])
+    dev = hoi.scan_device(covs, 3, 10)
+    path = dev.save(tmp_path / "cfg1.hoiscan", chunk_rows=100)
+    head, planes = hoi.read_scan(path)
+    assert head["n"] == 10 and head["g_end"] - head["g_begin"] == 968 and head["datasets"] == 1
+    np.testing.assert_array_equal(planes, dev.out.cpu().numpy())
+    np.testing.assert_allclose(planes[:, :, 0], g["vals"], rtol=RTOL, atol=ATOL)
