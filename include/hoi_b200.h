@@ -194,7 +194,9 @@ int hoi_lattice_filter(void *ws, int32_t N, int32_t D, int32_t d, const double *
                        int64_t cand_cap, uint64_t *count, void *stream);
 
 /* Block-sharded engine-2 scan (one process per GPU, no data-path
- * collective): shard `shard` of 2^shard_bits (shard_bits <= (N-10)/2) owns
+ * collective; replaces the reference's in-process thread pool over batches,
+ * ref:scanner.py:290-305, across GPUs, with scan's output semantics,
+ * ref:scanner.py:308-365): shard `shard` of 2^shard_bits (shard_bits <= (N-10)/2) owns
  * the log-det table blocks whose top shard_bits prefix-variable bits equal
  * `shard`, i.e. every n-plet whose intersection with variables
  * N-10-shard_bits..N-11 is that pattern.  It rebuilds only the table
@@ -239,7 +241,8 @@ int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double 
                     int64_t k, int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
                     int64_t *h_count, void *ws, void *stream);
 
-/* hoi_topk_select for all D datasets of a (n, D) plane at once (D <= 64;
+/* TopK.update for every dataset of a batch (ref:scanner.py:75-100):
+ * hoi_topk_select for all D datasets of a (n, D) plane at once (D <= 64;
  * 8-bit radix digits, per-dataset histograms): dataset d's candidate
  * positions go to cand[d * cand_cap ...] and their count to h_counts[d]
  * (HOST array of D).  ws: device workspace of >= D*256 + 4*D + 64 uint64. */
@@ -247,7 +250,8 @@ int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign,
                           int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
                           int64_t *h_counts, void *ws, void *stream);
 
-/* Exact k-th smallest key: the order-preserving 64-bit key of the k-th
+/* Exact k-th smallest key (the threshold step of TopK, ref:scanner.py:75-100):
+ * the order-preserving 64-bit key of the k-th
  * smallest sign*vals[p*D+d] over p < n (full radix select), written to
  * device memory *key_out; all-ones when n <= k.  Synchronous.  ws: device
  * workspace of at least 4096 uint64. */
