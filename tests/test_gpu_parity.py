@@ -522,3 +522,37 @@ def test_scan_file_round_trip(tmp_path, golden):
     assert head["n"] == 10 and head["g_end"] - head["g_begin"] == 968 and head["datasets"] == 1
     np.testing.assert_array_equal(planes, dev.out.cpu().numpy())
     np.testing.assert_allclose(planes[:, :, 0], g["vals"], rtol=RTOL, atol=ATOL)
+
+
+def test_topk_at_n32_largest_lattice():
+    """N = 32, orders 2..32 (4.29e9 n-plets, 2^22 table blocks, 34 GB log-det
+    table): the filtered TopK's entries are re-evaluated by the per-n-plet
+    engine (values within the FP64 tolerance), and none of 200,000
+    uniformly sampled n-plets beats the k-th entry."""
+    rng = np.random.default_rng(32)
+    c = workloads.randcorr(32, rng)
+    x = rng.standard_normal((4000, 32)) @ np.linalg.cholesky(c).T
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
+    k = 50
+    top = hoi.scan(covs, 2, 32, hoi.TopK("o", "min", k))[0]
+    assert len(top) == k
+    vals = [e.o for e in top]
+    assert vals == sorted(vals)
+    for order in sorted({e.order for e in top}):
+        sel = [e for e in top if e.order == order]
+        h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(32, indices=np.array([e.indices for e in sel])))
+        np.testing.assert_allclose(h.o[:, 0], [e.o for e in sel], rtol=RTOL, atol=ATOL)
+        np.testing.assert_allclose(h.tc[:, 0], [e.tc for e in sel], rtol=RTOL, atol=ATOL)
+    total = hoi.count_nplets(32, 2, 32)
+    ranks = torch.as_tensor(np.sort(rng.choice(total, size=200_000, replace=False)), device="cuda")
+    idx = torch.empty((ranks.numel(), 32), dtype=torch.int32, device="cuda")
+    orders = torch.empty(ranks.numel(), dtype=torch.int32, device="cuda")
+    _native.check(_native.lib().hoi_unrank_list(32, 2, 32, ranks.data_ptr(), ranks.numel(),
+                                                idx.data_ptr(), orders.data_ptr(),
+                                                _native.stream_handle(torch)), "unrank_list")
+    idx, orders = idx.cpu().numpy(), orders.cpu().numpy()
+    worst = vals[-1]
+    for kk in np.unique(orders):
+        rows = idx[orders == kk, :kk].astype(np.int64)
+        h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(32, indices=rows, check_unique=False))
+        assert (h.o[:, 0] >= worst - 1e-9).all()
