@@ -556,3 +556,30 @@ def test_topk_at_n32_largest_lattice():
         rows = idx[orders == kk, :kk].astype(np.int64)
         h = hoi.compute_hoi_batch(covs, hoi.NpletBatch(32, indices=rows, check_unique=False))
         assert (h.o[:, 0] >= worst - 1e-9).all()
+
+
+def test_chunked_replay_reuses_the_table(monkeypatch):
+    """A Callback scan at N = 24 (two-pass lattice) replayed in forced small
+    device chunks (partial rank ranges that reuse one log-det table through
+    compacted block lists) returns exactly the one-shot device output, batch
+    by batch in the reference's order."""
+    from paper_2501_03381_b200 import scanner
+    rng = np.random.default_rng(24)
+    c = workloads.randcorr(24, rng)
+    x = rng.standard_normal((1500, 24)) @ np.linalg.cholesky(c).T
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
+    lo, hi = 6, 11
+    full = hoi.scan_device(covs, lo, hi, engine=2).out[:, :, 0].cpu().numpy()
+    monkeypatch.setattr(scanner, "_chunk_rows", lambda *a, **k: 700_000)
+    got, sizes = [], []
+
+    def keep(batch, h):
+        sizes.append((batch.batch_size, int(h.order[0])))
+        got.append(np.stack([h.tc[:, 0], h.dtc[:, 0], h.o[:, 0], h.s[:, 0]]))
+
+    hoi.scan(covs, lo, hi, hoi.Callback(keep), batch_size=250_000)
+    got = np.concatenate(got, axis=1)
+    assert got.shape == full.shape
+    np.testing.assert_array_equal(got, full)
+    assert all(b <= 250_000 for b, _ in sizes)
+    assert [k for _, k in sizes] == sorted(k for _, k in sizes)
