@@ -135,9 +135,19 @@ __global__ void k_col_mean(const double *__restrict__ z, int64_t T, int N, int D
   if (lane == 0) mean[w] = s / (double)T;
 }
 
-// Tiled FP64 SYRK: 32x32 output tile per CTA (upper tiles only), 256
-// threads, each thread 4 outputs; the value is written to (i,j) and (j,i)
-// so the result is exactly symmetric.
+// X^T X on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): one 32 x 32
+// output tile per CTA (upper tiles only), its two 32-sample centred panels
+// staged in shared memory; 8 warps x 2 of the 16 8x8 sub-tiles, 8 MMA
+// k-steps of 4 samples per panel, FP64 accumulation throughout.  The value
+// of (i, j) is written to (i, j) and (j, i), so the covariance is exactly
+// symmetric (the reference symmetrises with 0.5 (S + S^T),
+// ref:copula_core.py:187-189).
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 __global__ void __launch_bounds__(256)
 k_cov(const double *__restrict__ z, const double *__restrict__ mean, int64_t T,
       int N, double *__restrict__ cov) {
@@ -149,12 +159,15 @@ k_cov(const double *__restrict__ z, const double *__restrict__ mean, int64_t T,
   int ti = 0, rem = tile;
   while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
   int tj = ti + rem;
-  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int lane = tx, warp = ty;
   const double *zd = z + (int64_t)d * T * N;
   const double *md = mean + (int64_t)d * N;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int ci = ti * 32 + tx, cj = tj * 32 + tx;
-  double mi = ci < N ? md[ci] : 0.0, mj = cj < N ? md[cj] : 0.0;
+  const int ci = ti * 32 + tx, cj = tj * 32 + tx;
+  const double mi = ci < N ? md[ci] : 0.0, mj = cj < N ? md[cj] : 0.0;
+  // warp -> sub-tile row block rb, column blocks cb0, cb0 + 1
+  const int rb = warp >> 1, cb0 = (warp & 1) * 2;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   for (int64_t t0 = 0; t0 < T; t0 += 32) {
     for (int r = ty; r < 32; r += 8) {
       int64_t t = t0 + r;
@@ -163,22 +176,31 @@ k_cov(const double *__restrict__ z, const double *__restrict__ mean, int64_t T,
       B[r][tx] = (ok && cj < N) ? zd[t * N + cj] - mj : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) {
-      double b = B[r][tx];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(A[r][ty + 8 * q], b, acc[q]);
+    for (int kk = 0; kk < 8; ++kk) {
+      const int r = 4 * kk + (lane & 3);
+      const double a = A[r][rb * 8 + (lane >> 2)];                 // A^T fragment (8 x 4, row)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double b = B[r][(cb0 + c) * 8 + (lane >> 2)];        // B fragment (4 x 8, col)
+        dmma_8x8x4(acc[c][0], acc[c][1], a, b);
+      }
     }
     __syncthreads();
   }
-  double inv = 1.0 / (double)(T - 1);
+  const double inv = 1.0 / (double)(T - 1);
   double *cd = cov + (int64_t)d * N * N;
-  for (int q = 0; q < 4; ++q) {
-    int i = ti * 32 + ty + 8 * q, j = tj * 32 + tx;
-    if (i < N && j < N && (ti < tj || i <= j)) {
-      double v = acc[q] * inv;
-      cd[(int64_t)i * N + j] = v;
-      cd[(int64_t)j * N + i] = v;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = ti * 32 + rb * 8 + (lane >> 2);
+      const int j = tj * 32 + (cb0 + c) * 8 + 2 * (lane & 3) + h;
+      if (i < N && j < N && (ti < tj || i <= j)) {
+        const double v = acc[c][h] * inv;
+        cd[(int64_t)i * N + j] = v;
+        cd[(int64_t)j * N + i] = v;
+      }
     }
   }
 }
