@@ -347,6 +347,13 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
                                        didx.data_ptr(), B, K, out.data_ptr(), None, None,
                                        cnt.data_ptr(), coords.data_ptr(), 64, s), "eval")
 
+    s32 = st.corr32
+
+    def ev32():
+        nat.check(lib.hoi_eval_indices_fp32(st.corr.data_ptr(), s32.data_ptr(), st.sdiag.data_ptr(),
+                                            None, 0, 400, D, didx.data_ptr(), B, K, out.data_ptr(),
+                                            cnt.data_ptr(), coords.data_ptr(), 64, s), "eval32")
+
     def ev_topk():
         ev()
         red = hoi.TopK("o", "min", 1000)
@@ -364,6 +371,14 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
     e[1].record()
     torch.cuda.synchronize()
     kms = e[0].elapsed_time(e[1]) / a.steps
+    ev32()
+    torch.cuda.synchronize()
+    e[0].record()
+    for _ in range(a.steps):
+        ev32()
+    e[1].record()
+    torch.cuda.synchronize()
+    kms32 = e[0].elapsed_time(e[1]) / a.steps
     t0 = time.perf_counter()
     for _ in range(3):
         ev_topk()
@@ -396,6 +411,8 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
         "value": units / (step_s),
         "kernel_only": units / (kms * 1e-3),
         "kernel_ms": kms, "step_ms_with_topk": step_s * 1e3,
+        "fp32_fast_path": {"kernel_ms": kms32, "units_per_s": units / (kms32 * 1e-3),
+                           "tolerance": "1e-4 nats absolute vs FP64 (tests/test_gpu_parity.py)"},
         "e2e": {"value": units / e2e_s, "seconds_per_step": e2e_s,
                 "h2d_bytes_per_step": int(idx.size * 4 + sig.nbytes),
                 "d2h_bytes_per_step": int(len(res) * 1000 * (8 * 5 + 8 * K)),

@@ -130,6 +130,18 @@ int hoi_eval_masks(const double *corr, const double *sdiag, const double *eta,
 /* Raw matrix stack: (logdet, inverse diagonal) of M matrices (M, K, K) with
  * the same jitter rule.  Replaces _batched_logdet_invdiag
  * (ref:nplet_engine.py:267-281); err_coords hold (m, 0). */
+/* FP32 fast path of hoi_eval_indices (the north star's optional FP32 path,
+ * within 1e-4 nats of the FP64 result): the same units, gathered from corr32
+ * (an FP32 copy of corr) and factorised in FP32 for orders K <= 16 (log
+ * products, bias and the epilogue stay FP64; a failing pivot reruns that unit
+ * on the FP64 path with the reference's jitter rule); orders above 16 run
+ * the FP64 kernels.  Measures only (no log det / inverse-diagonal outputs). */
+int hoi_eval_indices_fp32(const double *corr, const float *corr32, const double *sdiag,
+                          const double *eta, int32_t kstride, int32_t N, int32_t D,
+                          const int32_t *idx, int64_t B, int32_t K, double *out,
+                          int32_t *err_count, int64_t *err_coords, int32_t err_cap,
+                          void *stream);
+
 int hoi_logdet_invdiag(const double *mats, int64_t M, int32_t K,
                        double *logdet, double *invdiag, int32_t *err_count,
                        int64_t *err_coords, int32_t err_cap, void *stream);

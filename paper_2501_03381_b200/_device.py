@@ -26,6 +26,14 @@ class DeviceCovs:
                                             self.sdiag.data_ptr(), nat.stream_handle(torch)),
                   "correlation")
         self._eta = {}
+        self._corr32 = None
+
+    @property
+    def corr32(self):
+        """FP32 copy of the correlation form (the FP32 fast path's gather source)."""
+        if self._corr32 is None:
+            self._corr32 = self.corr.float()
+        return self._corr32
 
     def eta(self, k_max: int):
         """(D, k_max+1) bias table on the device (host-evaluated with scipy,

@@ -37,6 +37,8 @@ _SIGS = {
     "hoi_correlation": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "hoi_eval_indices": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                           _vp, _i32, _vp], C.c_int),
+    "hoi_eval_indices_fp32": ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp,
+                               _vp, _i32, _vp], C.c_int),
     "hoi_eval_masks": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _i64, _vp, _vp, _vp, _vp,
                         _vp, _i32, _vp], C.c_int),
     "hoi_logdet_invdiag": ([_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp], C.c_int),

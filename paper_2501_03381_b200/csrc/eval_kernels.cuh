@@ -55,6 +55,8 @@ struct EvalArgs {
   int32_t *err_count;
   int64_t *err_coords;
   int err_cap;
+  const float *src32;      // FP32 copy of the correlation (FP32 fast path) or nullptr
+  int fp32;                // 1: factorise in FP32 (log products and epilogue in FP64)
 };
 
 #define TRI(i, j) ((i) * ((i) + 1) / 2 + (j))
@@ -79,12 +81,12 @@ __device__ __forceinline__ void unrank_lex(uint64_t r, int K, int N, int *s) {
 // copy for small N x N x D -- or the raw matrix stack in mats mode.  The
 // correlation form has an exact unit diagonal (k_corr writes 1.0), so only
 // the strict lower triangle is gathered.
-template <int KT, bool FIXED>
-__device__ __forceinline__ void load_matrix(const EvalArgs &A, const double *__restrict__ src,
+template <int KT, bool FIXED, typename TM = double>
+__device__ __forceinline__ void load_matrix(const EvalArgs &A, const TM *__restrict__ src,
                                             int64_t b, int d, int K,
-                                            const int (&s)[KT], double (&a)[KT * (KT + 1) / 2],
+                                            const int (&s)[KT], TM (&a)[KT * (KT + 1) / 2],
                                             bool jitter) {
-  if (A.mats) {
+  if (A.mats) {   // (FP64 only)
     const double *m = A.src + (int64_t)b * K * K;
     double tr = 0.0;
 #pragma unroll
@@ -105,10 +107,10 @@ __device__ __forceinline__ void load_matrix(const EvalArgs &A, const double *__r
   const int N = A.N, D = A.D;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const double *row = src + (s[i] * N) * D + d;
+    const TM *row = src + (s[i] * N) * D + d;
 #pragma unroll
     for (int j = 0; j < i; ++j) a[TRI(i, j)] = row[s[j] * D];
-    a[TRI(i, i)] = 1.0;
+    a[TRI(i, i)] = TM(1);
   }
   if (jitter) {
     double tr = 0.0;
@@ -134,8 +136,11 @@ __device__ __forceinline__ void load_matrix(const EvalArgs &A, const double *__r
 // Rows are updated bottom-up so the unscaled column j stays readable without
 // a temporary copy (fewer live registers -> more resident warps); the
 // reciprocal is __drcp_rn, bit-identical to 1.0 / d.
-template <int KT, bool FIXED, bool STORE_CS>
-__device__ __forceinline__ bool ldl_invdiag(double (&a)[KT * (KT + 1) / 2], int K,
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+
+template <int KT, bool FIXED, bool STORE_CS, typename TM = double>
+__device__ __forceinline__ bool ldl_invdiag(TM (&a)[KT * (KT + 1) / 2], int K,
                                             double (&cs)[KT], double &l, double &lam) {
   // the diagonal slot of column j holds 1/d_j once the column is done, so
   // the packed triangle is the only K x K state (fewer live registers)
@@ -143,15 +148,15 @@ __device__ __forceinline__ bool ldl_invdiag(double (&a)[KT * (KT + 1) / 2], int 
   pd.init();
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const double dj = a[TRI(j, j)];
-    if (!(dj > 0.0)) return false;
-    pd.mul(dj);
+    const TM dj = a[TRI(j, j)];
+    if (!(dj > TM(0))) return false;
+    pd.mul((double)dj);
     if ((j & 7) == 7) pd.renorm();
-    const double r = __drcp_rn(dj);
+    const TM r = rcp_rn(dj);
     a[TRI(j, j)] = r;
 #pragma unroll
     for (int i = K - 1; i > j; --i) {
-      const double lij = a[TRI(i, j)] * r;
+      const TM lij = a[TRI(i, j)] * r;
 #pragma unroll
       for (int m = j + 1; m <= i; ++m) a[TRI(i, m)] = fma(-lij, a[TRI(m, j)], a[TRI(i, m)]);
       a[TRI(i, j)] = lij;
@@ -163,7 +168,7 @@ __device__ __forceinline__ bool ldl_invdiag(double (&a)[KT * (KT + 1) / 2], int 
   for (int j = 0; j < K; ++j) {
 #pragma unroll
     for (int i = j + 1; i < K; ++i) {
-      double acc = a[TRI(i, j)];
+      TM acc = a[TRI(i, j)];
 #pragma unroll
       for (int m = j + 1; m < i; ++m) acc = fma(a[TRI(i, m)], a[TRI(m, j)], acc);
       a[TRI(i, j)] = -acc;
@@ -174,14 +179,14 @@ __device__ __forceinline__ bool ldl_invdiag(double (&a)[KT * (KT + 1) / 2], int 
   pl.init();
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    double sacc = a[TRI(j, j)];
+    TM sacc = a[TRI(j, j)];
 #pragma unroll
     for (int i = j + 1; i < K; ++i) {
-      const double u = a[TRI(i, j)];
+      const TM u = a[TRI(i, j)];
       sacc = fma(u * u, a[TRI(i, i)], sacc);
     }
-    if (STORE_CS) cs[j] = sacc;
-    pl.mul(sacc);
+    if (STORE_CS) cs[j] = (double)sacc;
+    pl.mul((double)sacc);
     if ((j & 7) == 7) pl.renorm();
   }
   pl.renorm();
@@ -275,18 +280,24 @@ __device__ __noinline__ void eval_retry(const EvalArgs &A, const double *src, in
   finish_unit<KT, FIXED, COMPAT>(A, b, d, K, s, ok, l, lam, cs);
 }
 
-template <int KT, bool FIXED, bool COMPAT>
-__device__ __forceinline__ void eval_unit(const EvalArgs &A, const double *src, int64_t b, int d,
+// TM = float: the FP32 fast path (factorisation in FP32, log products and
+// the epilogue in FP64; a failing pivot reruns the unit through the FP64
+// path with the reference's jitter rule).
+template <int KT, bool FIXED, bool COMPAT, typename TM = double>
+__device__ __forceinline__ void eval_unit(const EvalArgs &A, const TM *src, int64_t b, int d,
                                           int kdyn) {
   const int K = FIXED ? KT : kdyn;
   int s[KT];
   unit_indices<KT, FIXED>(A, b, K, s);
-  double a[KT * (KT + 1) / 2];
+  TM a[KT * (KT + 1) / 2];
   double cs[KT];
   double l = 0.0, lam = 0.0;
-  load_matrix<KT, FIXED>(A, src, b, d, K, s, a, false);
-  if (!ldl_invdiag<KT, FIXED, COMPAT>(a, K, cs, l, lam)) {
-    eval_retry<KT, FIXED, COMPAT>(A, src, b, d, K);
+  load_matrix<KT, FIXED, TM>(A, src, b, d, K, s, a, false);
+  if (!ldl_invdiag<KT, FIXED, COMPAT, TM>(a, K, cs, l, lam)) {
+    if constexpr (sizeof(TM) == sizeof(double))
+      eval_retry<KT, FIXED, COMPAT>(A, reinterpret_cast<const double *>(src), b, d, K);
+    else
+      eval_retry<KT, FIXED, COMPAT>(A, A.src, b, d, K);
     return;
   }
   finish_unit<KT, FIXED, COMPAT>(A, b, d, K, s, true, l, lam, cs);
@@ -304,13 +315,18 @@ struct EvalOcc {
 // Grid-stride over (n-plet, dataset) units, dataset fastest.  SMEM: the
 // whole correlation matrix (small N x N x D, e.g. 7.2 KB for N = 30) is
 // staged once per CTA and gathered from shared memory instead of L1/L2.
-template <int KT, bool FIXED, bool COMPAT, bool SMEM>
+template <int KT, bool FIXED, bool COMPAT, bool SMEM, typename TM = double>
 __global__ void __launch_bounds__(128, EvalOcc<KT>::value) k_eval(const EvalArgs A, int kdyn) {
-  extern __shared__ double sR[];
-  const double *src = A.src;
+  extern __shared__ __align__(16) unsigned char sRraw[];
+  TM *sR = reinterpret_cast<TM *>(sRraw);
+  const TM *src;
+  if constexpr (sizeof(TM) == sizeof(double))
+    src = reinterpret_cast<const TM *>(A.src);
+  else
+    src = reinterpret_cast<const TM *>(A.src32);
   if (SMEM) {
     const int n = A.N * A.N * A.D;
-    for (int x = threadIdx.x; x < n; x += blockDim.x) sR[x] = __ldg(A.src + x);
+    for (int x = threadIdx.x; x < n; x += blockDim.x) sR[x] = __ldg(src + x);
     __syncthreads();
     src = sR;
   }
@@ -319,40 +335,47 @@ __global__ void __launch_bounds__(128, EvalOcc<KT>::value) k_eval(const EvalArgs
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = t / A.D;
     const int d = (int)(t - b * A.D);
-    eval_unit<KT, FIXED, COMPAT>(A, src, b, d, kdyn);
+    eval_unit<KT, FIXED, COMPAT, TM>(A, src, b, d, kdyn);
   }
 }
 
 constexpr int kEvalSmemMax = 48 * 1024;
 
-template <int KT, bool FIXED, bool COMPAT, bool SMEM>
+template <int KT, bool FIXED, bool COMPAT, bool SMEM, typename TM = double>
 static int launch_k(const EvalArgs &A, int K, int64_t n, cudaStream_t s) {
-  const int smem = SMEM ? (int)(sizeof(double) * A.N * A.N * A.D) : 0;
+  const int smem = SMEM ? (int)(sizeof(TM) * A.N * A.N * A.D) : 0;
   static thread_local int cap_for = -1, cap = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (cap_for != dev) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<KT, FIXED, COMPAT, SMEM>, 128,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<KT, FIXED, COMPAT, SMEM, TM>, 128,
                                                   SMEM ? kEvalSmemMax : 0);
     cap = sms * (per > 0 ? per : 1);
     cap_for = dev;
   }
   const int64_t want = (n + 127) / 128;
   const int grid = (int)(want < cap ? want : cap);
-  k_eval<KT, FIXED, COMPAT, SMEM><<<grid, 128, smem, s>>>(A, K);
+  k_eval<KT, FIXED, COMPAT, SMEM, TM><<<grid, 128, smem, s>>>(A, K);
   return check_launch("k_eval");
 }
 
 // WITH_COMPAT: also instantiate the entropy_terms variant (log det and the
 // inverse diagonal in Sigma space); large fixed orders route it to the
 // runtime-K kernel instead (compile time).
-template <int KT, bool FIXED, bool WITH_COMPAT = true>
+template <int KT, bool FIXED, bool WITH_COMPAT = true, bool WITH_FP32 = false>
 static int launch_one(const EvalArgs &A, int K, cudaStream_t s) {
   int64_t n = A.B * (int64_t)A.D;
   if (n == 0) return HOI_OK;
   const bool compat = A.logdet || A.invdiag;
+  if constexpr (WITH_FP32) {
+    if (A.fp32 && A.src32 && !compat && !A.mats) {
+      const bool sm32 = sizeof(float) * A.N * A.N * A.D <= (size_t)kEvalSmemMax;
+      return sm32 ? launch_k<KT, FIXED, false, true, float>(A, K, n, s)
+                  : launch_k<KT, FIXED, false, false, float>(A, K, n, s);
+    }
+  }
   const bool smem = !A.mats && sizeof(double) * A.N * A.N * A.D <= (size_t)kEvalSmemMax;
   if (compat) {
     if (!WITH_COMPAT) return -1;

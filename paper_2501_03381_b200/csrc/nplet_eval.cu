@@ -101,6 +101,24 @@ extern "C" int hoi_eval_indices(const double *corr, const double *sdiag, const d
   return launch_eval(A, K, (cudaStream_t)stream);
 }
 
+extern "C" int hoi_eval_indices_fp32(const double *corr, const float *corr32,
+                                     const double *sdiag, const double *eta, int32_t kstride,
+                                     int32_t N, int32_t D, const int32_t *idx, int64_t B,
+                                     int32_t K, double *out, int32_t *err_count,
+                                     int64_t *err_coords, int32_t err_cap, void *stream) {
+  HOI_CHECK_ARG(corr && corr32 && idx && err_count && out && N >= 1 && D >= 1 && B >= 0,
+                "hoi_eval_indices_fp32: bad args");
+  HOI_CHECK_ARG(K >= 1 && K <= 64 && K <= N, "hoi_eval_indices_fp32: bad order");
+  HOI_CHECK_ARG(!eta || kstride > K, "hoi_eval_indices_fp32: bias table too short");
+  EvalArgs A{};
+  A.src = corr; A.src32 = corr32; A.fp32 = 1; A.sdiag = sdiag; A.eta = eta; A.kstride = kstride;
+  A.N = N; A.D = D; A.mats = 0; A.idx = idx; A.idx_stride = K; A.row_map = nullptr;
+  A.B = B; A.r0 = 0; A.out = out; A.plane = B * (int64_t)D; A.out_row0 = 0;
+  A.logdet = nullptr; A.invdiag = nullptr; A.inv_n = 0;
+  A.err_count = err_count; A.err_coords = err_coords; A.err_cap = err_cap;
+  return launch_eval(A, K, (cudaStream_t)stream);
+}
+
 extern "C" int hoi_logdet_invdiag(const double *mats, int64_t M, int32_t K, double *logdet,
                                   double *invdiag, int32_t *err_count, int64_t *err_coords,
                                   int32_t err_cap, void *stream) {

@@ -220,9 +220,13 @@ def _batched_logdet_invdiag(mats: np.ndarray):
 
 
 def eval_device(covs: CovSet, batch: NpletBatch, bias_correct: bool, *, measures: bool = True,
-                terms: bool = False):
+                terms: bool = False, precision: str = "fp64"):
     """Run the fused per-n-plet kernel on a batch.  Returns device tensors
-    (out (4, B, D) or None, logdet (B, D) or None, invdiag or None)."""
+    (out (4, B, D) or None, logdet (B, D) or None, invdiag or None).
+    precision="fp32": the FP32 fast path (index batches, measures only;
+    within 1e-4 nats of FP64)."""
+    if precision not in ("fp64", "fp32"):
+        raise InvalidData(f"precision must be 'fp64' or 'fp32', got {precision!r}")
     _check_batch(covs, batch)
     st = device_covs(covs)
     torch = st.torch
@@ -240,6 +244,14 @@ def eval_device(covs: CovSet, batch: NpletBatch, bias_correct: bool, *, measures
             logdet = torch.empty((b, d), dtype=torch.float64, device="cuda")
             invdiag = torch.empty((b, d, k), dtype=torch.float64, device="cuda")
         idx = torch.from_numpy(batch.indices.astype(np.int32)).cuda()
+        if precision == "fp32" and measures and not terms:
+            nat.check(lib.hoi_eval_indices_fp32(st.corr.data_ptr(), st.corr32.data_ptr(),
+                                                st.sdiag.data_ptr(), nat.ptr(eta), kstride, n, d,
+                                                idx.data_ptr(), b, k, out.data_ptr(), cnt.data_ptr(),
+                                                coords.data_ptr(), ERR_CAP,
+                                                nat.stream_handle(torch)), "eval_indices_fp32")
+            _raise_not_pd(cnt, coords)
+            return out, None, None
         nat.check(lib.hoi_eval_indices(st.corr.data_ptr(), st.sdiag.data_ptr(), nat.ptr(eta),
                                        kstride, n, d, idx.data_ptr(), b, k, nat.ptr(out),
                                        nat.ptr(logdet), nat.ptr(invdiag), cnt.data_ptr(),

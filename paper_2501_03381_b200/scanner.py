@@ -751,7 +751,8 @@ class _BatchCtx:
         self.d, self.torch = d, torch
 
 
-def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: bool = False):
+def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: bool = False,
+               precision: str = "fp64"):
     """``reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct))``
     with the selection on the device (ref:scanner.py:75-100 semantics):
     the four measures of the batch stay in HBM, a radix select per dataset
@@ -762,7 +763,8 @@ def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: 
     if not isinstance(reducer, TopK):
         raise InvalidData("topk_batch needs a TopK reducer")
     from .nplet_engine import eval_device
-    out, _, _ = eval_device(covs, batch, bias_correct, measures=True, terms=False)
+    out, _, _ = eval_device(covs, batch, bias_correct, measures=True, terms=False,
+                            precision=precision)
     ctx = _BatchCtx(out.shape[2], nat.torch_cuda())
 
     def tuples_of(pos):

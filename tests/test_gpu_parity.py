@@ -583,3 +583,27 @@ def test_chunked_replay_reuses_the_table(monkeypatch):
     np.testing.assert_array_equal(got, full)
     assert all(b <= 250_000 for b, _ in sizes)
     assert [k for _, k in sizes] == sorted(k for _, k in sizes)
+
+
+@pytest.mark.parametrize("n,k,d", [(400, 10, 16), (30, 16, 1), (30, 6, 1), (30, 20, 1)])
+def test_fp32_fast_path_within_1e4_nats(n, k, d):
+    """precision='fp32' (FP32 factorisation, FP64 logs and epilogue) stays
+    within the north star's 1e-4 nats of the FP64 path; orders above 16 run
+    the FP64 kernels (identical)."""
+    if n == 400:
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(i)))
+                           for i in range(d)])
+        idx = workloads.cfg5_nplets(b=50_000, n=n, k=k)
+    else:
+        covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
+        rng = np.random.default_rng(k)
+        idx = np.sort(np.argsort(rng.random((20_000, n)), axis=1)[:, :k], axis=1)
+    batch = hoi.NpletBatch(n, indices=idx, check_unique=False)
+    for bias in (False, True):
+        h64 = hoi.compute_hoi_batch(covs, batch, bias_correct=bias)
+        h32 = hoi.compute_hoi_batch(covs, batch, bias_correct=bias, precision="fp32")
+        for m in ("tc", "dtc", "o", "s"):
+            err = np.abs(getattr(h32, m) - getattr(h64, m)).max()
+            assert err < 1e-4, (m, err)
+            if k > 16:
+                assert err == 0.0
