@@ -1167,14 +1167,14 @@ int lattice_fused(const double *corr, int N, int D, int d, const double *eta, in
 }
 
 int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_bytes,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool reset_flag = true) {
   size_t need = 0;
   int st = lattice_ws_bytes(N, D, &need);
   if (st) return st;
   if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
   upload_tables();
   LatticeWs w = ws_view(ws, N);
-  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+  if (reset_flag) cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
   k_lattice_table<8><<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag, 0u);
@@ -1491,10 +1491,23 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
                       int kmax, int64_t g_begin, int64_t g_end, double *out, int32_t *err_count,
                       void *ws, size_t ws_bytes, cudaStream_t s) {
   (void)err_count;
-  // Sequential table -> stencil measured faster on B200 (25.0 ms for cfg4)
-  // than the chunked two-stream pipeline (26.1 ms); lattice_pipeline stays
-  // available for the measurements in DESIGN.md.
+  // Sequential table -> stencil per dataset (the chunked two-stream
+  // pipeline measured no gain).  The not-PD flag is checked
+  // once after every dataset (one host sync per scan, not per dataset): a
+  // failing table leaves garbage rows, and HOI_FALLBACK makes the host rerun
+  // the whole scan on the per-n-plet engine with the reference's jitter rule.
   static const int pipe = getenv("HOI_PIPE") ? atoi(getenv("HOI_PIPE")) : 0;
+  if (!pipe) {
+    LatticeWs w = ws_view(ws, N);
+    cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+    for (int d = 0; d < D; ++d) {
+      int st = lattice_table(corr, N, D, d, ws, ws_bytes, s, false);
+      if (st) return st;
+      st = lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, s);
+      if (st) return st;
+    }
+    return lattice_status(ws, N, s);
+  }
   for (int d = 0; d < D; ++d) {
     if (pipe) {
       int st = lattice_pipeline(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
