@@ -38,7 +38,6 @@ constexpr int BLK = 1 << CB;      // 1024 table entries per block
 constexpr int LANE_BITS = 5;      // F0..F4 -> lane, F5..F9 -> register recursion
 constexpr int MAXV = 32;          // max variables
 constexpr int MAXB = 6;           // prefix variables expanded inside one CTA
-constexpr double LN2 = 0.69314718055994530942;
 // Schur pivots of a correlation matrix lie in (0, 1]; a pivot below this
 // means R is (numerically) singular and the table would carry rounding
 // noise, so the engine declines and the per-n-plet engine (with the
@@ -48,6 +47,42 @@ constexpr double kMinPivot = 1e-12;
 // (126 MB / 8 KB blocks ~ 2^14 blocks): streamed with evict-first loads.
 constexpr int kFarBits = 6;
 constexpr int kMinNearBits = 12;
+
+// Measurement knobs of the lattice engine, read once from the environment.
+// The defaults are the measured best on B200 (cfg4); the
+// alternatives stay selectable so those measurements can be repeated.
+//   HOI_RING 4|5|6          stencil ring slots per CTA (4: 4 CTAs x 4 slots)
+//   HOI_OWN_LAST 0|1        own block loaded with L2 evict_last
+//   HOI_NEAR_BITS b         neighbour bits >= b loaded evict-first (default: none)
+//   HOI_TWO_PASS 0|1        two-pass stencil for full output (N >= 24)
+//   HOI_TWO_PASS_FILTER 0|1 two-pass stencil for the TopK filter
+//   HOI_PREFETCH 0|1        claim-ahead L2 prefetch of DRAM-sourced blocks
+//   HOI_PIPE 0|1 (+ HOI_PIPE_WB, HOI_TABLE_NW, HOI_STENCIL_PER_SM)
+//                           chunked two-stream table/stencil pipeline
+struct LatticeTuning {
+  int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
+  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3;
+  LatticeTuning() {
+    auto get = [](const char *name, int &v) {
+      if (const char *e = getenv(name)) v = atoi(e);
+    };
+    get("HOI_RING", ring);
+    get("HOI_OWN_LAST", own_last);
+    get("HOI_NEAR_BITS", near_bits);
+    get("HOI_TWO_PASS", two_pass);
+    get("HOI_TWO_PASS_FILTER", two_pass_filter);
+    get("HOI_PREFETCH", prefetch);
+    get("HOI_PIPE", pipe);
+    get("HOI_PIPE_WB", pipe_wb);
+    get("HOI_TABLE_NW", table_nw);
+    get("HOI_STENCIL_PER_SM", stencil_per_sm);
+  }
+};
+
+const LatticeTuning &tuning() {
+  static const LatticeTuning t;
+  return t;
+}
 
 __constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
@@ -1245,13 +1280,12 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     int st = check_launch("k_block_active");
     if (st) return st;
   }
-  // experiment knobs (defaults are the measured best)
   // measured on B200 (cfg4): 4 CTAs x 4-slot rings beat 3 x 6 (17.8 ms) and
   // 2 x 10 (20.7 ms) -- more independent in-order streams per SM; own block
-  // evict_last
-  static const int ring = getenv("HOI_RING") ? atoi(getenv("HOI_RING")) : 4;
-  static const int own_last = getenv("HOI_OWN_LAST") ? atoi(getenv("HOI_OWN_LAST")) : 1;
-  if (getenv("HOI_NEAR_BITS")) near_bits = atoi(getenv("HOI_NEAR_BITS"));
+  // evict_last (tuning(), top of file)
+  const int ring = tuning().ring;
+  const int own_last = tuning().own_last;
+  if (tuning().near_bits >= 0) near_bits = tuning().near_bits;
   const int64_t plane = (g_end - g_begin) * (int64_t)D;
   const int nP = N - CB;
   const unsigned all = (1u << nP) - 1u;
@@ -1266,15 +1300,15 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   // (DRAM 68.8 vs 84.2 GB); the filtered (TopK) pass writes nothing and is
   // bound by per-job TMA latency rather than bytes, so there the single pass
   // wins (11.4 ms vs 3.4 + 9.6 ms).
-  static const int two_env = getenv("HOI_TWO_PASS") ? atoi(getenv("HOI_TWO_PASS")) : 1;
-  static const int two_flt = getenv("HOI_TWO_PASS_FILTER") ? atoi(getenv("HOI_TWO_PASS_FILTER")) : 0;
+  const int two_env = tuning().two_pass;
+  const int two_flt = tuning().two_pass_filter;
   const bool two = (flt ? two_flt : two_env) && nP >= 14 && blk_begin == 0 &&
                    blk_end == (1u << nP) && w.lowsum;
   const int lb = nP / 2;
   const StencilFilter none{};
   // claim-ahead L2 prefetch of the own / pass-1-sum blocks: measured no
   // gain on B200 (cfg4 19.75-19.89 ms with vs 19.16 without), off
-  static const int pf = getenv("HOI_PREFETCH") ? atoi(getenv("HOI_PREFETCH")) : 0;
+  const int pf = tuning().prefetch;
   StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr, pf};
   // partial / sampled scans over the whole block space: compacted block
   // lists (natural order for a single pass or pass 1, high-bits-fastest for
@@ -1447,9 +1481,9 @@ int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta,
   LatticeWs w = ws_view(ws, N);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
-  static const int wb_env = getenv("HOI_PIPE_WB") ? atoi(getenv("HOI_PIPE_WB")) : 16;
-  static const int tnw = getenv("HOI_TABLE_NW") ? atoi(getenv("HOI_TABLE_NW")) : 4;
-  static const int sper = getenv("HOI_STENCIL_PER_SM") ? atoi(getenv("HOI_STENCIL_PER_SM")) : 3;
+  const int wb_env = tuning().pipe_wb;
+  const int tnw = tuning().table_nw;
+  const int sper = tuning().stencil_per_sm;
   const int wb = nP < wb_env ? nP : wb_env;         // chunk = 2^wb blocks
   const int nchunks = 1 << (nP - wb);
   int64_t h_off[MAXV + 1];
@@ -1496,7 +1530,7 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
   // once after every dataset (one host sync per scan, not per dataset): a
   // failing table leaves garbage rows, and HOI_FALLBACK makes the host rerun
   // the whole scan on the per-n-plet engine with the reference's jitter rule.
-  static const int pipe = getenv("HOI_PIPE") ? atoi(getenv("HOI_PIPE")) : 0;
+  const int pipe = tuning().pipe;
   if (!pipe) {
     LatticeWs w = ws_view(ws, N);
     cudaMemsetAsync(w.flag, 0, sizeof(int), s);
