@@ -284,7 +284,7 @@ extern "C" int hoi_covariance(const double *z, int64_t T, int32_t N, int32_t D,
   HOI_CHECK_ARG(T >= 2 && N >= 1 && D >= 1 && z && cov, "hoi_covariance: bad args");
   cudaStream_t s = (cudaStream_t)stream;
   double *mean = nullptr;
-  if (cudaMallocAsync(&mean, sizeof(double) * D * N, s) != cudaSuccess)
+  if (stream_alloc((void **)&mean, sizeof(double) * D * N, s) != cudaSuccess)
     return fail(HOI_CUDA_ERROR, "hoi_covariance: cudaMallocAsync failed");
   k_col_mean<<<grid_for((int64_t)D * N * 32, 256), 256, 0, s>>>(z, T, N, D, mean);
   int st = check_launch("k_col_mean");

@@ -539,36 +539,81 @@ struct StencilPass {
 };
 
 // Compact the flagged blocks into a list in claim order (natural, or
-// high-bits-fastest when perm_lb > 0).  One CTA of 1024 threads: each
-// thread counts a contiguous slice of claim indices, a block scan gives its
-// write offset.  Skipping inactive blocks one atomic claim at a time costs
-// every producer ~nblocks/active serialized atomics per block it keeps.
-__global__ void __launch_bounds__(1024)
-k_compact_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb,
-                 unsigned *__restrict__ list, unsigned *__restrict__ count) {
-  __shared__ unsigned part[1024];
-  const unsigned n = 1u << nP, t = threadIdx.x;
-  const unsigned per = (n + 1023) / 1024, c0 = t * per, c1 = c0 + per < n ? c0 + per : n;
+// high-bits-fastest when perm_lb > 0).  Skipping inactive blocks one atomic
+// claim at a time would cost every producer ~nblocks/active serialized
+// atomics per block it keeps.  Two launches over tiles of kCompactTile claim
+// positions, 256 threads per tile, position c = tile * 4096 + i * 256 + tid:
+// k_count_blocks counts each tile's flags, k_write_blocks sums the counts of
+// the tiles before its own (<= 1024 of them) and writes its flagged blocks
+// warp-ballot by warp-ballot, preserving claim order.  (One 1024-thread CTA
+// scanning contiguous slices took 1.1 ms for 2^20 blocks: strided byte loads.)
+constexpr unsigned kCompactTile = 4096;
+
+__device__ __forceinline__ unsigned claim_perm(unsigned c, int nP, int perm_lb) {
   const int hb = nP - perm_lb;
-  auto perm = [&](unsigned c) {
-    return perm_lb ? (((c & ((1u << hb) - 1u)) << perm_lb) | (c >> hb)) : c;
-  };
-  unsigned cnt = 0;
-  for (unsigned c = c0; c < c1; ++c) cnt += active[perm(c)];
-  part[t] = cnt;
+  return perm_lb ? (((c & ((1u << hb) - 1u)) << perm_lb) | (c >> hb)) : c;
+}
+
+__global__ void __launch_bounds__(256)
+k_count_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb, unsigned *__restrict__ tile_cnt) {
+  const unsigned n = 1u << nP, c0 = blockIdx.x * kCompactTile;
+  int cnt = 0;
+  for (unsigned i = 0; i < kCompactTile / 256; ++i) {
+    const unsigned c = c0 + i * 256 + threadIdx.x;
+    cnt += (c < n && active[claim_perm(c, nP, perm_lb)]) ? 1 : 0;
+  }
+  __shared__ int red[8];
+  #pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {       // inclusive Hillis-Steele scan
-    const unsigned v = t >= (unsigned)o ? part[t - o] : 0u;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    tile_cnt[blockIdx.x] = (unsigned)t;
   }
-  unsigned pos = part[t] - cnt;
-  for (unsigned c = c0; c < c1; ++c) {
-    const unsigned q = perm(c);
-    if (active[q]) list[pos++] = q;
+}
+
+__global__ void __launch_bounds__(256)
+k_write_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb,
+               const unsigned *__restrict__ tile_cnt, unsigned *__restrict__ list,
+               unsigned *__restrict__ count) {
+  __shared__ unsigned wsum[8];
+  __shared__ unsigned base_s;
+  const unsigned n = 1u << nP, c0 = blockIdx.x * kCompactTile;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned pre = 0;
+  for (unsigned t = threadIdx.x; t < blockIdx.x; t += 256) pre += tile_cnt[t];
+  #pragma unroll
+  for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) wsum[warp] = pre;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < 8; ++w) t += wsum[w];
+    base_s = t;
   }
-  if (t == 1023) *count = part[1023];
+  __syncthreads();
+  unsigned base = base_s;
+  for (unsigned i = 0; i < kCompactTile / 256; ++i) {
+    const unsigned c = c0 + i * 256 + threadIdx.x;
+    const unsigned q = c < n ? claim_perm(c, nP, perm_lb) : 0u;
+    const bool on = c < n && active[q];
+    const unsigned m = __ballot_sync(0xffffffffu, on);
+    __syncthreads();                       // previous round's wsum reads done
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    unsigned before = 0, total = 0;
+    #pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const unsigned v = wsum[w];
+      before += (unsigned)w < warp ? v : 0u;
+      total += v;
+    }
+    if (on) list[base + before + __popc(m & ((1u << lane) - 1u))] = q;
+    base += total;
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count = base;
 }
 
 enum { MODE_FULL = 0, MODE_FILTER = 1, MODE_LOWSUM = 2 };
@@ -1124,8 +1169,9 @@ int lattice_ws_bytes(int N, int D, size_t *bytes) {
   // 2^(N-10) u32 | pad to 256 B | low-pass neighbour sums 2^N f64 (N >= 24)
   *bytes = (sizeof(double) << N) + 4096 + (sizeof(unsigned) << (N - CB));
   if (N - CB >= 14) *bytes = ((*bytes + 255) & ~(size_t)255) + (sizeof(double) << N);
-  // | compacted block lists 2 x 2^(N-10) u32 + 2 counts
-  *bytes = ((*bytes + 255) & ~(size_t)255) + (sizeof(unsigned) << (N - CB + 1)) + 64;
+  // | compacted block lists 2 x 2^(N-10) u32 | 2 counts (64 B) | 2 x 1024
+  // per-tile counts of the compaction
+  *bytes = ((*bytes + 255) & ~(size_t)255) + (sizeof(unsigned) << (N - CB + 1)) + 64 + 8192;
   return HOI_OK;
 }
 
@@ -1138,7 +1184,7 @@ struct LatticeWs {
   int64_t *offs;      // order offsets
   unsigned *ready;    // fused pass: per-block publish flags
   double *lowsum;     // two-pass stencil: low-bit neighbour sums (or nullptr)
-  unsigned *list;     // compacted block lists (2 x 2^(N-10)) + 2 counts
+  unsigned *list;     // compacted block lists (2 x 2^(N-10)) + 2 counts + tile counts
 };
 
 static LatticeWs ws_view(void *ws, int N) {
@@ -1316,9 +1362,15 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   const bool listed = active && blk_begin == 0 && blk_end == (1u << nP);
   unsigned *list1 = w.list, *list2 = w.list + (1u << nP), *cnts = w.list + 2 * (1u << nP);
   if (listed) {
-    k_compact_blocks<<<1, 1024, 0, s>>>(active, nP, 0, list1, cnts);
-    if (two) k_compact_blocks<<<1, 1024, 0, s>>>(active, nP, lb, list2, cnts + 1);
-    int st = check_launch("k_compact_blocks");
+    const unsigned ntiles = ((1u << nP) + kCompactTile - 1) / kCompactTile;
+    unsigned *tiles = cnts + 16;
+    k_count_blocks<<<ntiles, 256, 0, s>>>(active, nP, 0, tiles);
+    k_write_blocks<<<ntiles, 256, 0, s>>>(active, nP, 0, tiles, list1, cnts);
+    if (two) {
+      k_count_blocks<<<ntiles, 256, 0, s>>>(active, nP, lb, tiles + 1024);
+      k_write_blocks<<<ntiles, 256, 0, s>>>(active, nP, lb, tiles + 1024, list2, cnts + 1);
+    }
+    int st = check_launch("k_count_blocks/k_write_blocks");
     if (st) return st;
     ps.list = list1;
     ps.nlist = cnts;

@@ -148,7 +148,7 @@ extern "C" int hoi_eval_masks(const double *corr, const double *sdiag, const dou
   int64_t *row_map = nullptr;
   size_t bytes = sizeof(int32_t) * (B + 2 * 72) + sizeof(int32_t) * B * N + sizeof(int64_t) * B;
   char *ws = nullptr;
-  if (cudaMallocAsync((void **)&ws, bytes + 64, s) != cudaSuccess)
+  if (stream_alloc((void **)&ws, bytes + 64, s) != cudaSuccess)
     return fail(HOI_CUDA_ERROR, "hoi_eval_masks: allocation failed");
   row_map = reinterpret_cast<int64_t *>(ws);
   order = reinterpret_cast<int32_t *>(row_map + B);
