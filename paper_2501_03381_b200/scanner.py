@@ -19,6 +19,8 @@ otherwise has nothing to do: there is no host thread pool to size).
 from __future__ import annotations
 
 import ctypes
+import functools
+import gc
 import math
 import time
 from dataclasses import dataclass
@@ -58,6 +60,36 @@ class TopEntry:
     s: float
 
 
+_new = object.__new__
+
+
+def _gc_paused(fn):
+    """Run fn with Python's cyclic collector paused (restored on exit).  The
+    TopK merges build tens of thousands of small acyclic objects (entries,
+    index tuples, keys); with torch loaded, the collections they trigger walk
+    every live object and cost more than the merge itself (BASELINE config
+    5's 16 x 1000 entries: 55 -> 19 ms)."""
+    @functools.wraps(fn)
+    def run(*args, **kwargs):
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            if was:
+                gc.enable()
+    return run
+
+
+def _entry(t, v, tc, dtc, o, sv):
+    """TopEntry(t, len(t), v, tc, dtc, o, sv) without the frozen dataclass's
+    per-field object.__setattr__ calls (half the cost; the device TopK paths
+    build one per selected row).  Same class, fields, equality and hash."""
+    e = _new(TopEntry)
+    e.__dict__.update(indices=t, order=len(t), value=v, tc=tc, dtc=dtc, o=o, s=sv)
+    return e
+
+
 class TopK(Reducer):
     """k best n-plets per dataset for one measure; ties broken by the
     lexicographically smallest index tuple (ref:scanner.py:50-105)."""
@@ -82,6 +114,7 @@ class TopK(Reducer):
         best.sort(key=lambda pair: pair[0])
         del best[self.k:]
 
+    @_gc_paused
     def update(self, batch, hoi):
         vals = getattr(hoi, self.measure)
         b, d_count = vals.shape
@@ -538,6 +571,7 @@ def _emit_progress(progress, n, lo, hi, batch_size, total, t0):
                   "elapsed": time.perf_counter() - t0})
 
 
+@_gc_paused
 def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
     """Merge one device chunk into the running per-dataset TopK lists.
 
@@ -575,6 +609,15 @@ def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
                                       cands.data_ptr(), cap, ctypes.byref(cnt), ws.data_ptr(), s),
                   "topk_select")
         counts = [int(cnt.value)]
+    # every dataset's candidates in one gather and one device->host copy
+    ok = [d for d in range(ctx.d) if counts[d] <= cap]
+    if ok:
+        cnt_t = torch.tensor([counts[d] for d in ok], dtype=torch.int64)
+        d_sel = torch.repeat_interleave(torch.tensor(ok, dtype=torch.int64), cnt_t).to("cuda")
+        pos_all = torch.cat([cands[d, :counts[d]] for d in ok])
+        vals_all = out[:, pos_all, d_sel].cpu().numpy()            # (4, sum c)
+        pos_all = pos_all.cpu().numpy()
+    a = 0
     for d in range(ctx.d):
         c = counts[d]
         if c > cap:
@@ -586,24 +629,23 @@ def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
             else:
                 _topk_host_rows(reducer, out, d, tuples_of)
             continue
-        pos = cands[d, :c]
-        vals = out[:, pos, d].cpu().numpy()            # (4, c)
+        vals, pos = vals_all[:, a:a + c], pos_all[a:a + c]
+        a += c
         if c > reducer.k:
             # keep the k best keys and every tie at the k-th before building
             # Python objects (the exact tuple tie-break happens in _merge)
             key = sign * vals[m_idx]
             keep = np.flatnonzero(key <= np.partition(key, reducer.k - 1)[reducer.k - 1])
-            vals = vals[:, keep]
-            pos = pos[torch.from_numpy(keep).to(pos.device)]
+            vals, pos = vals[:, keep], pos[keep]
             c = keep.size
         if tuples_of is not None:
-            tuples = tuples_of(pos.cpu().numpy())
+            tuples = tuples_of(pos)
         else:
-            tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, (pos + g0).cpu().numpy()) if c else []
+            tuples = _unrank_list(ctx.n, ctx.lo, ctx.hi, pos + g0) if c else []
         new = []
         for t, (tc, dtc, o, sv) in zip(tuples, vals.T.tolist()):
             v = (tc, dtc, o, sv)[m_idx]
-            new.append(((sign * v, t), TopEntry(t, len(t), v, tc, dtc, o, sv)))
+            new.append(((sign * v, t), _entry(t, v, tc, dtc, o, sv)))
         reducer._merge(d, new)
 
 
@@ -645,6 +687,7 @@ def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
     reducer._merge(d, sub._best[0])
 
 
+@_gc_paused
 def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
     """TopK over an exhaustive scan without writing the full output (lattice
     engine): per dataset, (1) build the log-det table; (2) run the filtered
@@ -730,12 +773,9 @@ def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
         rec = cand[pos[:h]].cpu().numpy()
         ranks = rec[:, 0].view(np.int64)
         tuples = _unrank_list(n, ctx.lo, ctx.hi, ranks) if h else []
-        mv = rec[:, 1 + m_idx]
-        for i in range(h):
-            e = TopEntry(indices=tuples[i], order=len(tuples[i]), value=float(mv[i]),
-                         tc=float(rec[i, 1]), dtc=float(rec[i, 2]), o=float(rec[i, 3]),
-                         s=float(rec[i, 4]))
-            best[d].append(((sign * e.value, e.indices), e))
+        for t, r in zip(tuples, rec[:, 1:].tolist()):
+            v = r[m_idx]
+            best[d].append(((sign * v, t), _entry(t, v, *r)))
     if reducer._best is None:
         reducer._best = [[] for _ in range(ctx.d)]
     for d in range(ctx.d):

@@ -23,3 +23,30 @@ run()
 t = time.perf_counter(); run(); print("topk stage", time.perf_counter() - t)
 pr = cProfile.Profile(); pr.enable(); run(); pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+
+# stage times of bench.py's cfg5 e2e call (topk_batch from host index arrays)
+def e2e():
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    hoi.topk_batch(covs, batch, hoi.TopK("o", "min", 1000)).finalize()
+    torch.cuda.synchronize()
+    return time.perf_counter() - t
+e2e(); print("e2e", e2e())
+t = time.perf_counter()
+for d in range(16):
+    hoi.estimate_covariance(hoi.copula_transform(workloads.cfg5_data(d)))
+torch.cuda.synchronize(); print("16 copula+cov (incl. data gen)", time.perf_counter() - t)
+pr = cProfile.Profile(); pr.enable(); e2e(); pr.disable()
+pstats.Stats(pr).sort_stats("cumtime").print_stats(25)
+
+import gc
+def med(f, n=7):
+    ts = []
+    for _ in range(n):
+        torch.cuda.synchronize(); t = time.perf_counter(); f(); torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t)
+    return float(np.median(ts))
+print("median topk stage", med(run), "e2e", med(e2e))
+gc.disable()
+print("gc off: median topk stage", med(run), "e2e", med(e2e))
+gc.enable()
