@@ -1,0 +1,361 @@
+// Engine 1, orders 17..32: G threads per (n-plet, dataset) unit, 32/G units
+// per warp, the whole factorisation in registers with compile-time indices.
+//
+// Thread t of a group owns rows i = t + G*m (m < M, KT = G*M >= K).  Row
+// slot m is stored padded to G*(m+1) columns, so every register index is a
+// compile-time (m, column) pair and the thread id only enters predicates and
+// shared-memory addresses -- the matrix stays in registers (a packed
+// triangle indexed by a runtime row went to local memory).  Orders K < KT
+// are padded with identity rows: pivots 1, no updates, log 1 = 0.
+//
+//   LDL^T, right-looking: step j publishes column j (each thread its rows'
+//   entries) to a per-unit shared vector; every thread reads the pivot and
+//   the column back as broadcasts and updates a[i][l] -= l_ij a[l][j] for
+//   its rows (entries right of a row's diagonal are scratch).
+//   W = L^-1 in place, right-looking: step j publishes row j of W (final by
+//   then), rows i > j apply w[i][c] -= l_ij w[j][c] and set w[i][j] = -l_ij.
+//   (R_S^-1)_cc = sum_i w[i][c]^2 / d_i: per-thread column partials go
+//   through shared memory, thread t sums the columns c = t (mod G) it owns.
+//
+// Work per unit ~ KT^3/3 FMAs spread over G lanes (the warp-per-unit kernel
+// issues ~KT^2 warp-wide FMAs per unit with half its lanes idle or on the
+// scratch half).  Failure rule as the other kernels (ref
+// nplet_engine.py:237-264): a non-positive pivot retries the unit once with
+// the jittered diagonal; a second failure records (row, dataset) and writes
+// NaN.
+#include "eval_kernels.cuh"
+
+namespace hoib {
+namespace {
+
+constexpr int kGWarps = 4;   // warps per CTA
+
+template <int G, int M>
+struct GrpSmem {                       // one per unit (group)
+  double vec[2][G * M + 2];            // broadcast vector, double-buffered by step parity
+  double red[G][G * M + 1];            // column partials of the inverse diagonal
+  int idx[G * M];                      // variable ids of the unit's n-plet
+};
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v, unsigned gmask) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+  return v;
+}
+
+template <int G, int M, bool COMPAT, bool SMEM>
+__global__ void __launch_bounds__(32 * kGWarps, 1) k_eval_grp(const EvalArgs A, int K) {
+  constexpr int KT = G * M, U = 32 / G, S = G * M * (M + 1) / 2;
+  extern __shared__ __align__(16) double dynR[];
+  __shared__ __align__(16) GrpSmem<G, M> usm[kGWarps * U];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = lane % G, g = lane / G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (g * G);
+  const int N = A.N, D = A.D;
+  const double *src = A.src;
+  if (SMEM) {
+    const int n = N * N * D;
+    for (int x = threadIdx.x; x < n; x += blockDim.x) dynR[x] = __ldg(A.src + x);
+    __syncthreads();
+    src = dynR;
+  }
+  GrpSmem<G, M> &sm = usm[w * U + g];
+  // each group takes a contiguous chunk of units (dataset fastest): in
+  // unranking mode it unranks once, then steps to the lexicographic successor
+  const int64_t units = A.B * (int64_t)D;
+  const int64_t ng = (int64_t)gridDim.x * kGWarps * U;
+  const int64_t gid = ((int64_t)blockIdx.x * kGWarps + w) * U + g;
+  const int64_t per = (units + ng - 1) / ng;
+  const int64_t u_begin = gid * per, u_end = u_begin + per < units ? u_begin + per : units;
+  int64_t cur_b = -1;
+  for (int64_t u = u_begin; u < u_end; ++u) {
+    const int64_t b = u / D;
+    const int d = (int)(u - b * D);
+    // ------------------------------------------------------------ indices ----
+    if (b != cur_b) {
+      __syncwarp(gmask);                       // previous unit's idx reads done
+      if (A.idx) {
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          if (t + G * m < K) sm.idx[t + G * m] = A.idx[b * A.idx_stride + t + G * m];
+      } else if (t == 0) {
+        if (cur_b >= 0 && b == cur_b + 1) {
+          // successor: the rightmost position p with s[p] < N - K + p is
+          // incremented, the positions after it follow consecutively
+          int p = K - 1;
+          while (p > 0 && sm.idx[p] >= N - K + p) --p;
+          const int v = sm.idx[p] + 1;
+          for (int q = p; q < K; ++q) sm.idx[q] = v + (q - p);
+        } else {
+          uint64_t r = A.r0 + (uint64_t)b;
+          int c = 0;
+          for (int p = 0; p < K; ++p) {
+            while (c < N) {
+              const uint64_t bb = binom_l1(N - 1 - c, K - 1 - p);
+              if (bb <= r) {
+                r -= bb;
+                ++c;
+              } else {
+                break;
+              }
+            }
+            sm.idx[p] = c++;
+          }
+        }
+      }
+      cur_b = b;
+      __syncwarp(gmask);
+    }
+    int si[M];
+    double sg[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int i = t + G * m;
+      si[m] = i < K ? sm.idx[i] : 0;
+      sg[m] = (A.sdiag && i < K) ? A.sdiag[(int64_t)d * N + si[m]] : 1.0;
+    }
+    bool ok = false;
+    double l = 0.0, lam = 0.0;
+    double inv[M];
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+      // ----------------------------------------------------------- gather ----
+      double a[S];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int i = t + G * m;
+        const double *row = src + ((int64_t)si[m] * N) * D + d;
+#pragma unroll
+        for (int c = 0; c < G * (m + 1); ++c) {
+          double v = c == i ? 1.0 : 0.0;
+          if (c < i && i < K) v = row[(int64_t)sm.idx[c] * D];
+          a[G * m * (m + 1) / 2 + c] = v;
+        }
+      }
+      if (attempt == 1) {   // the reference's jitter: Sigma_S + eps I, eps = 1e-10 tr / K
+        double tr = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) tr += t + G * m < K ? sg[m] : 0.0;
+        tr = A.sdiag ? group_sum<G>(tr, gmask) : (double)K;
+        const double eps = 1e-10 * tr / (double)K;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int i = t + G * m;
+#pragma unroll
+          for (int c = 0; c < G * (m + 1); ++c)
+            if (c == i && i < K) a[G * m * (m + 1) / 2 + c] += eps / sg[m];
+        }
+      }
+      // -------------------------------------------------------------- LDL ----
+      LogProd pd;
+      pd.init();
+      bool good = true;
+      double dinv[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) dinv[m] = 1.0;
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        if (j < K) {
+          double *vec = sm.vec[j & 1];
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+            if (G * (m + 1) > j) vec[t + G * m] = a[G * m * (m + 1) / 2 + j];
+          __syncwarp(gmask);
+          const double dj = vec[j];
+          if (!(dj > 0.0)) {
+            good = false;
+            break;
+          }
+          pd.mul(dj);
+          if ((j & 7) == 7) pd.renorm();
+          const double rp = __drcp_rn(dj);
+          if (t == j % G) dinv[j / G] = rp;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            if (G * (m + 1) > j + 1) {         // the slot has rows below j
+              const int o = G * m * (m + 1) / 2;
+              const double lij = a[o + j] * rp;
+#pragma unroll
+              for (int c = (j + 1) & ~1; c < G * (m + 1); c += 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(vec + c);
+                if (c > j) a[o + c] = fma(-lij, v.x, a[o + c]);
+                a[o + c + 1] = fma(-lij, v.y, a[o + c + 1]);
+              }
+              a[o + j] = lij;
+            }
+          }
+        }
+      }
+      if (!good) {
+        __syncwarp(gmask);
+        continue;
+      }
+      pd.renorm();
+      l = pd.log_value();
+      __syncwarp(gmask);                       // last LDL step's broadcast reads done
+      // ------------------------------------------------- W = L^-1 in place ----
+#pragma unroll
+      for (int j = 1; j < KT; ++j) {
+        if (j < K) {
+          double *vec = sm.vec[j & 1];
+          if (t == j % G) {                    // row j of W is final: publish it
+#pragma unroll
+            for (int c = 0; c < j; c += 2) {
+              const int q = G * (j / G) * (j / G + 1) / 2 + c;
+              if (c + 1 < j)
+                *reinterpret_cast<double2 *>(vec + c) = make_double2(a[q], a[q + 1]);
+              else
+                vec[c] = a[q];
+            }
+          }
+          __syncwarp(gmask);
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            if (G * (m + 1) > j + 1) {
+              const int o = G * m * (m + 1) / 2;
+              if (t + G * m > j) {
+                const double lij = a[o + j];
+#pragma unroll
+                for (int c = 0; c < j; c += 2) {
+                  const double2 v = *reinterpret_cast<const double2 *>(vec + c);
+                  a[o + c] = fma(-lij, v.x, a[o + c]);
+                  if (c + 1 < j) a[o + c + 1] = fma(-lij, v.y, a[o + c + 1]);
+                }
+                a[o + j] = -lij;
+              }
+            }
+          }
+        }
+      }
+      // ------------------------------- (R^-1)_cc = sum_i w_ic^2 / d_i ----
+#pragma unroll
+      for (int c = 0; c < KT; ++c) {
+        double p = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          if (G * (m + 1) > c) {
+            const int i = t + G * m;
+            const double wv = c < i ? a[G * m * (m + 1) / 2 + c] : (c == i ? 1.0 : 0.0);
+            p = fma(wv * wv, dinv[m], p);
+          }
+        }
+        sm.red[t][c] = p;
+      }
+      __syncwarp(gmask);
+      double ls = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int c = t + G * m;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < G; ++q) s += sm.red[q][c];
+        inv[m] = s;
+        if (c < K) ls += log(s);
+      }
+      lam = group_sum<G>(ls, gmask);
+      ok = true;
+      __syncwarp(gmask);
+    }
+    // ------------------------------------------------------------- output ----
+    const int64_t ob = A.row_map ? A.row_map[b] : A.out_row0 + b;
+    const int64_t o = ob * D + d;
+    if (!ok) {
+      if (t == 0) {
+        const int slot = atomicAdd(A.err_count, 1);
+        if (slot < A.err_cap) {
+          A.err_coords[2 * slot] = ob;
+          A.err_coords[2 * slot + 1] = d;
+        }
+        const double nan = __longlong_as_double(0x7ff8000000000000ll);
+        if (A.out)
+          for (int q = 0; q < 4; ++q) A.out[q * A.plane + o] = nan;
+        if (COMPAT && A.logdet) A.logdet[o] = nan;
+      }
+      continue;
+    }
+    if (A.out && t == 0) {
+      double tc, dtc, oi;
+      const double kd = (double)K;
+      if (A.eta) {
+        const double *e = A.eta + (int64_t)d * A.kstride;
+        const double e1 = e[1], ek = e[K], ek1 = e[K - 1];
+        tc = -0.5 * l - kd * e1 + ek;
+        dtc = 0.5 * (l + lam) + (kd - 1.0) * ek - kd * ek1;
+        oi = -l - 0.5 * lam - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+      } else {
+        tc = -0.5 * l;
+        dtc = 0.5 * (l + lam);
+        oi = -l - 0.5 * lam;
+      }
+      A.out[o] = tc;
+      A.out[A.plane + o] = dtc;
+      A.out[2 * A.plane + o] = oi;
+      A.out[3 * A.plane + o] = tc + dtc;
+    }
+    if (COMPAT) {
+      // Sigma-space values (entropy_terms compat)
+      double lsg = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int c = t + G * m;
+        if (c < K) {
+          if (A.sdiag) lsg += log(sg[m]);
+          if (A.invdiag) {
+            const double v = inv[m] / sg[m];
+            if (A.inv_n > 0)
+              A.invdiag[o * A.inv_n + si[m]] = v;
+            else
+              A.invdiag[o * K + c] = v;
+          }
+        }
+      }
+      lsg = group_sum<G>(lsg, gmask);
+      if (A.logdet && t == 0) A.logdet[o] = l + lsg;
+    }
+  }
+}
+
+template <int G, int M, bool COMPAT, bool SMEM>
+int launch_grp(const EvalArgs &A, int K, cudaStream_t s) {
+  auto kern = k_eval_grp<G, M, COMPAT, SMEM>;
+  const int smem = SMEM ? (int)(sizeof(double) * A.N * A.N * A.D) : 0;
+  static thread_local int cap_for = -1, cap = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cap_for != dev) {
+    if (SMEM) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvalSmemMax);
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * kGWarps, SMEM ? kEvalSmemMax : 0);
+    cap = sms * (per > 0 ? per : 1);
+    cap_for = dev;
+  }
+  constexpr int per_cta = kGWarps * (32 / G);
+  const int64_t n = A.B * (int64_t)A.D;
+  const int64_t want = (n + per_cta - 1) / per_cta;
+  const int grid = (int)(want < cap ? want : cap);
+  kern<<<grid, 32 * kGWarps, smem, s>>>(A, K);
+  return check_launch("k_eval_grp");
+}
+
+template <int G, int M>
+int pick_grp(const EvalArgs &A, int K, bool compat, bool smem, cudaStream_t s) {
+  if (compat) return smem ? launch_grp<G, M, true, true>(A, K, s) : launch_grp<G, M, true, false>(A, K, s);
+  return smem ? launch_grp<G, M, false, true>(A, K, s) : launch_grp<G, M, false, false>(A, K, s);
+}
+
+}  // namespace
+
+int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s) {
+  if (K < 17 || K > 32 || A.mats) return -1;
+  upload_binomials();
+  const int64_t n = A.B * (int64_t)A.D;
+  if (n == 0) return HOI_OK;
+  const bool compat = A.logdet || A.invdiag;
+  const bool smem = sizeof(double) * A.N * A.N * A.D <= (size_t)kEvalSmemMax;
+  if (K <= 20) return pick_grp<4, 5>(A, K, compat, smem, s);
+  if (K <= 24) return pick_grp<8, 3>(A, K, compat, smem, s);
+  return pick_grp<8, 4>(A, K, compat, smem, s);
+}
+
+}  // namespace hoib

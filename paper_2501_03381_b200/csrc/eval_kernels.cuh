@@ -390,5 +390,6 @@ int launch_eval_k1_12(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_k13_16(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_generic(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_warp(const EvalArgs &A, int K, cudaStream_t s);   // 17 <= K <= 32
+int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s);  // 17 <= K <= 32
 
 }  // namespace hoib

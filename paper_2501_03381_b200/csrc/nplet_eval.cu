@@ -1,5 +1,7 @@
 // Engine 1 host side: dispatch, unranking, mask compaction and the C ABI.
 // The per-unit kernels live in eval_kernels.cuh (see there).
+#include <cstdlib>
+
 #include "eval_kernels.cuh"
 
 namespace hoib {
@@ -9,7 +11,15 @@ int launch_eval(const EvalArgs &A, int K, cudaStream_t s) {
   int st = -1;
   if (K <= 12) st = launch_eval_k1_12(A, K, s);
   else if (K <= 16) st = launch_eval_k13_16(A, K, s);
-  else if (K <= 32) st = launch_eval_warp(A, K, s);
+  else if (K <= 32) {
+    // 17..32: G threads per unit (registers, compile-time indices); the
+    // warp-per-unit kernel stays selectable for comparison (HOI_EVAL_WARP=1)
+    static const bool warp = [] {
+      const char *e = getenv("HOI_EVAL_WARP");
+      return e && atoi(e) != 0;
+    }();
+    st = warp ? launch_eval_warp(A, K, s) : launch_eval_group(A, K, s);
+  }
   return st >= 0 ? st : launch_eval_generic(A, K, s);
 }
 

@@ -336,6 +336,35 @@ def _random_cov(n, seed):
     return r * np.outer(d, d)
 
 
+@pytest.mark.parametrize("k", [17, 19, 20, 21, 24, 25, 29, 32])
+def test_mid_orders_vs_oracle(oracle, k):
+    """Orders 17..32 (the G-threads-per-unit kernels, KT = 20 / 24 / 32 with
+    identity padding): index batches over 3 datasets with non-unit variances,
+    with and without bias; log det / inverse-diagonal terms; and unranking
+    mode (every order-k n-plet of N = k + 3 variables on engine 1)."""
+    n, d, t = 40, 3, 900
+    sig = np.stack([_random_cov(n, 100 + k + s) for s in range(d)])
+    sig = 0.5 * (sig + sig.transpose(0, 2, 1))
+    rng = np.random.default_rng(k)
+    idx = np.sort(np.stack([rng.choice(n, k, replace=False) for _ in range(300)]), axis=1)
+    covs = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=t) for s in sig])
+    batch = hoi.NpletBatch(n, indices=idx)
+    for bias in (False, True):
+        h = hoi.compute_hoi_batch(covs, batch, bias_correct=bias)
+        want = oracle.hoi_batch(sig, [t] * d, idx=idx, bias=bias)
+        np.testing.assert_allclose(np.stack([h.tc, h.dtc, h.o, h.s]), np.stack(want[:4]),
+                                   rtol=RTOL, atol=ATOL)
+    terms = hoi.entropy_terms(covs, batch)
+    xj, _, xl = oracle.terms_fixed(sig, [t] * d, idx)
+    np.testing.assert_allclose(terms.excess_joint, xj, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(terms.excess_leave_one_out, xl, rtol=1e-12, atol=1e-12)
+    m = k + 3
+    small = hoi.CovSet([hoi.CovarianceMatrix(sig[0, :m, :m], n_samples_used=t)])
+    dev = hoi.scan_device(small, k, k, bias_correct=True, engine=1)
+    _, vals = oracle.scan(sig[:1, :m, :m], [t], k, k, oracle.CollectR(), bias=True)
+    np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
+
+
 @pytest.mark.parametrize("engine", [2, 3])
 @pytest.mark.parametrize("n,lo,hi", [(12, 1, 12), (13, 2, 13), (16, 3, 9)])
 @pytest.mark.parametrize("bias", [False, True])
