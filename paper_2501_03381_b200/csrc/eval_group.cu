@@ -31,7 +31,7 @@ namespace {
 constexpr int kGWarps = 4;   // warps per CTA
 
 template <int G, int M>
-struct GrpSmem {                       // one per unit (group)
+struct __align__(16) GrpSmem {         // one per unit (group); 16-byte vector accesses
   double vec[2][G * M + 2];            // broadcast vector, double-buffered by step parity
   double red[G][G * M + 1];            // column partials of the inverse diagonal
   int idx[G * M];                      // variable ids of the unit's n-plet
@@ -44,8 +44,8 @@ __device__ __forceinline__ double group_sum(double v, unsigned gmask) {
   return v;
 }
 
-template <int G, int M, bool COMPAT, bool SMEM>
-__global__ void __launch_bounds__(32 * kGWarps, 1) k_eval_grp(const EvalArgs A, int K) {
+template <int G, int M, int MINB, bool COMPAT, bool SMEM>
+__global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs A, int K) {
   constexpr int KT = G * M, U = 32 / G, S = G * M * (M + 1) / 2;
   extern __shared__ __align__(16) double dynR[];
   __shared__ __align__(16) GrpSmem<G, M> usm[kGWarps * U];
@@ -315,9 +315,9 @@ __global__ void __launch_bounds__(32 * kGWarps, 1) k_eval_grp(const EvalArgs A, 
   }
 }
 
-template <int G, int M, bool COMPAT, bool SMEM>
+template <int G, int M, int MINB, bool COMPAT, bool SMEM>
 int launch_grp(const EvalArgs &A, int K, cudaStream_t s) {
-  auto kern = k_eval_grp<G, M, COMPAT, SMEM>;
+  auto kern = k_eval_grp<G, M, MINB, COMPAT, SMEM>;
   const int smem = SMEM ? (int)(sizeof(double) * A.N * A.N * A.D) : 0;
   static thread_local int cap_for = -1, cap = 0;
   int dev = 0;
@@ -338,10 +338,11 @@ int launch_grp(const EvalArgs &A, int K, cudaStream_t s) {
   return check_launch("k_eval_grp");
 }
 
-template <int G, int M>
+template <int G, int M, int MINB>
 int pick_grp(const EvalArgs &A, int K, bool compat, bool smem, cudaStream_t s) {
-  if (compat) return smem ? launch_grp<G, M, true, true>(A, K, s) : launch_grp<G, M, true, false>(A, K, s);
-  return smem ? launch_grp<G, M, false, true>(A, K, s) : launch_grp<G, M, false, false>(A, K, s);
+  if (compat)
+    return smem ? launch_grp<G, M, MINB, true, true>(A, K, s) : launch_grp<G, M, MINB, true, false>(A, K, s);
+  return smem ? launch_grp<G, M, MINB, false, true>(A, K, s) : launch_grp<G, M, MINB, false, false>(A, K, s);
 }
 
 }  // namespace
@@ -353,9 +354,15 @@ int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s) {
   if (n == 0) return HOI_OK;
   const bool compat = A.logdet || A.invdiag;
   const bool smem = sizeof(double) * A.N * A.N * A.D <= (size_t)kEvalSmemMax;
-  if (K <= 20) return pick_grp<4, 5>(A, K, compat, smem, s);
-  if (K <= 24) return pick_grp<8, 3>(A, K, compat, smem, s);
-  return pick_grp<8, 4>(A, K, compat, smem, s);
+  // (G, M) per order range, measured on B200 (cfg4 order segments, TF/s):
+  // K 17-18 (2,9) 3.2-3.7 | 19-20 (4,5) 3.8-4.3 | 21-24 (4,6) 3.9-4.9 |
+  // 25-28 (4,7) 3.1 (a little spilled, still 20% over (8,4)) | 29-32 (8,4).
+  // (8,3) for 21-24 ran 2.7-3.4; the warp-per-unit kernel 0.8-1.5.
+  if (K <= 18) return pick_grp<2, 9, 1>(A, K, compat, smem, s);
+  if (K <= 20) return pick_grp<4, 5, 1>(A, K, compat, smem, s);
+  if (K <= 24) return pick_grp<4, 6, 1>(A, K, compat, smem, s);
+  if (K <= 28) return pick_grp<4, 7, 1>(A, K, compat, smem, s);
+  return pick_grp<8, 4, 1>(A, K, compat, smem, s);
 }
 
 }  // namespace hoib
