@@ -365,6 +365,30 @@ def test_mid_orders_vs_oracle(oracle, k):
     np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
 
 
+def test_mixed_masks_high_orders_vs_oracle(oracle):
+    """Mixed-order mask batches reaching orders 17..32 (compacted per order,
+    rows scattered back, inverse diagonal scattered by variable id)."""
+    n, t = 34, 700
+    sig = _random_cov(n, 77)
+    sig = 0.5 * (sig + sig.T)
+    rng = np.random.default_rng(5)
+    orders = rng.integers(2, 33, size=240)
+    masks = np.zeros((orders.size, n), dtype=bool)
+    for r, k in enumerate(orders):
+        masks[r, rng.choice(n, int(k), replace=False)] = True
+    covs = hoi.CovSet([hoi.CovarianceMatrix(sig, n_samples_used=t)])
+    batch = hoi.NpletBatch(n, masks=masks)
+    for bias in (False, True):
+        h = hoi.compute_hoi_batch(covs, batch, bias_correct=bias)
+        want = oracle.hoi_batch(sig, [t], masks=masks, bias=bias)
+        np.testing.assert_allclose(np.stack([h.tc, h.dtc, h.o, h.s]), np.stack(want[:4]),
+                                   rtol=RTOL, atol=ATOL)
+    terms = hoi.entropy_terms(covs, batch)
+    xj, _, xl, _ = oracle.terms_mixed(sig[None], [t], masks)
+    np.testing.assert_allclose(terms.excess_joint, xj, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(terms.excess_leave_one_out, xl, rtol=1e-12, atol=1e-12)
+
+
 @pytest.mark.parametrize("engine", [2, 3])
 @pytest.mark.parametrize("n,lo,hi", [(12, 1, 12), (13, 2, 13), (16, 3, 9)])
 @pytest.mark.parametrize("bias", [False, True])
