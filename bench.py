@@ -57,6 +57,16 @@ def dist_env():
     return world, rank, local
 
 
+def max_over_ranks(torch, v: float) -> float:
+    """Max of a per-rank float (NCCL: through a device tensor; the gloo
+    smoke-test backend: a host tensor)."""
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------ CPU side --
 
 def cpu_sample(batches_per_order: int, workers: int):
@@ -242,6 +252,44 @@ def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
             "kernel_ms": tm, "table_kernel_ms": tt,
             "table_kernel_bytes": table_bytes,
             "kernel_share_of_step": (tm + tt) / step_ms}
+
+
+def shard_roofline(torch, nat, ctx, out, rank, sb, step_ms, steps):
+    """N > 1 (block shards): CUDA-event timing of this rank's whole shard
+    step (hoi_lattice_shard: its 1 + popc(rank) table chunks, then the
+    stencil over its own blocks), gathered from every rank; the slowest
+    rank is reported.  Algorithmic bytes of rank r: the table chunks it
+    writes and reads back (8 B x 2^(N-sb) each) + 32 B per n-plet it owns
+    (patterns of popcount p over the sb shard variables:
+    sum_k C(N - sb, k - p) rows)."""
+    import torch.distributed as dist
+    from paper_2501_03381_b200.sharding import allgather_objects
+    ts = []
+    for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        ctx.full_shard(rank, sb, out)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]))
+    t = float(np.mean(ts))
+    p = bin(rank).count("1")
+    chunk = 8 * (1 << (N - sb))
+    rows = sum(math.comb(N - sb, k - p) for k in range(LO, HI + 1) if 0 <= k - p <= N - sb)
+    alg = 2 * (1 + p) * chunk + 32 * rows
+    per = allgather_objects((t, alg, rank, rows))
+    t, alg, r, rows = max(per)
+    peak, src = measured_peaks()
+    achieved = alg / (t * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": f"hoi_lattice_shard of the slowest rank ({r} of {dist.get_world_size()}): "
+                      "its table chunks (k_lattice_table) + its stencil share "
+                      "(k_lattice_measures)",
+            "peak_source": src, "algorithmic_bytes_per_launch": alg,
+            "algorithmic_bytes_note": "table chunks written and read once (8 B x 2^(N-sb) "
+                                      "each) + 32 B x the rank's n-plets",
+            "kernel_ms": t, "rank_rows": rows, "kernel_share_of_step": t / step_ms}
 
 
 def fused_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
@@ -433,8 +481,10 @@ def b200_arm(a):
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # one rank per GPU; HOI_BENCH_BACKEND=gloo and the modulo exist only
+        # to smoke-test the multi-rank path on a one-GPU box (never timed)
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(os.environ.get("HOI_BENCH_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     import paper_2501_03381_b200 as hoi
@@ -470,7 +520,7 @@ def b200_arm(a):
         dist.barrier()
     launches0 = nat.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         e0.record()
         for _ in range(a.steps):
@@ -482,9 +532,7 @@ def b200_arm(a):
     ms = e0.elapsed_time(e1) / a.steps
     launches = (nat.launch_count() - launches0) // a.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(torch, ms)
     value = TOTAL / (ms * 1e-3)
 
     # roofline of the dominant kernel, timed per launch with CUDA events on
@@ -495,6 +543,8 @@ def b200_arm(a):
         roof = lattice_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     if rank == 0 and engine_used == 3:
         roof = fused_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
+    if sb is not None:
+        roof = shard_roofline(torch, nat, ctx, out, rank, sb, ms, a.steps)
     del out
     torch.cuda.empty_cache()
     fp64 = None
@@ -533,11 +583,13 @@ def b200_arm(a):
             line["cfg5_batched"] = cfg5_batched(a, torch, hoi, lib, nat, peak64)
         except Exception as exc:  # reported, never silently dropped
             line["cfg5_batched"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    if rank == 0 and not a.no_e2e:
+    if (rank == 0 or world > 1) and not a.no_e2e:
         try:
-            line["e2e"] = e2e(a, torch, hoi)
+            r = e2e(a, torch, hoi, world)       # every rank takes part when N > 1
         except Exception as exc:  # reported, never silently dropped
-            line["e2e"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            r = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if rank == 0:
+            line["e2e"] = r
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         v, sampled, spent = cpu_sample(os.cpu_count() or 1, os.cpu_count() or 1)
         line["cpu_baseline"] = {
@@ -551,9 +603,12 @@ def b200_arm(a):
         dist.destroy_process_group()
 
 
-def e2e(a, torch, hoi):
+def e2e(a, torch, hoi, world=1):
     """Public API end to end from pinned host memory: data -> copula ->
-    covariance -> scan(TopK('o','min',1000)) -> result on the host."""
+    covariance -> scan(TopK('o','min',1000)) -> result on the host.  N > 1:
+    every rank runs the same call through the multi-GPU entry point
+    (sharding.scan_sharded: its block shard, then the TopK merge across
+    ranks), each step timed from a barrier, max over ranks."""
     from paper_2501_03381_b200 import workloads
     x = workloads.cfg4()
     pinned = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
@@ -561,14 +616,25 @@ def e2e(a, torch, hoi):
     xh = pinned.numpy()
     times = []
     res = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2501_03381_b200.sharding import scan_sharded
     for i in range(1 + a.e2e_steps):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(hoi.DataMatrix(xh)))])
-        res = hoi.scan(covs, LO, HI, hoi.TopK("o", "min", 1000))
+        if world > 1:
+            res = scan_sharded(covs, LO, HI, hoi.TopK("o", "min", 1000))
+        else:
+            res = hoi.scan(covs, LO, HI, hoi.TopK("o", "min", 1000))
         torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            dt = max_over_ranks(torch, dt)
         if i:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
     t = float(np.median(times))
     h2d = x.nbytes + 8 * T + 8 * N * N
     d2h = 8 * N * N + len(res[0]) * (8 * 5 + 4 * HI)
