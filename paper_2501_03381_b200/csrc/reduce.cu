@@ -209,8 +209,8 @@ __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, i
 
 // 21-feature accumulator (ref:scanner.py:205-287), device part.  Pass 1:
 // thread t (grid stride a multiple of D, so one dataset per thread) walks
-// its rows in increasing rank order and keeps partials; pass 2: one
-// thread per dataset reduces the partials of that dataset in thread order
+// its rows in increasing rank order and keeps partials; pass 2: one CTA
+// per dataset merges that dataset's partials in a fixed order
 // (deterministic).  Fields per thread / per dataset:
 //  0 pair count, 1 sum tc (pairs), 2 sum tc^2 (pairs), 3 count (order >= 3),
 //  4..7 sum tc dtc o s, 8..11 max, 12..15 min, 16 first rank of the o max,
@@ -259,36 +259,57 @@ __global__ void k_features_partial(const double *__restrict__ out, int64_t rows,
   for (int i = 0; i < kFeat; ++i) p[i] = f[i];
 }
 
-__global__ void k_features_reduce(const double *__restrict__ part, int64_t nthreads, int D,
-                                  double *__restrict__ feat) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= D) return;
+// Merge partial p into f: sums add; max / min keep the larger / smaller
+// value, and for o an equal value keeps the smaller first-attainment rank,
+// so the merge is associative and commutative (order-independent).
+__device__ __forceinline__ void feat_merge(double *f, const double *p) {
+  for (int i = 0; i < 8; ++i) f[i] += p[i];
+  for (int m = 0; m < 4; ++m) {
+    if (p[8 + m] > f[8 + m] ||
+        (m == 2 && p[8 + m] == f[8 + m] && p[16] >= 0 && (f[16] < 0 || p[16] < f[16]))) {
+      f[8 + m] = p[8 + m];
+      if (m == 2) f[16] = p[16];
+    }
+    if (p[12 + m] < f[12 + m] ||
+        (m == 2 && p[12 + m] == f[12 + m] && p[17] >= 0 && (f[17] < 0 || p[17] < f[17]))) {
+      f[12 + m] = p[12 + m];
+      if (m == 2) f[17] = p[17];
+    }
+  }
+  f[18] += p[18];
+}
+
+// One CTA per dataset: thread i merges partials d + D*(i + 256 j) in j order,
+// then a fixed shared-memory tree -- the same summation order every run.
+constexpr int kFeatRed = 256;
+__global__ void __launch_bounds__(kFeatRed)
+k_features_reduce(const double *__restrict__ part, int64_t nthreads, int D,
+                  double *__restrict__ feat) {
+  __shared__ double sh[kFeatRed * kFeat];
+  const int d = blockIdx.x, i = threadIdx.x;
   double f[kFeat];
-  for (int i = 0; i < kFeat; ++i) f[i] = 0.0;
+  for (int q = 0; q < kFeat; ++q) f[q] = 0.0;
   for (int m = 0; m < 4; ++m) {
     f[8 + m] = -INFINITY;
     f[12 + m] = INFINITY;
   }
   f[16] = f[17] = -1.0;
-  for (int64_t t = d; t < nthreads; t += D) {
-    const double *p = part + t * kFeat;
-    for (int i = 0; i < 8; ++i) f[i] += p[i];
-    for (int m = 0; m < 4; ++m) {
-      // max: larger wins, equal values keep the smaller first-attainment rank
-      if (p[8 + m] > f[8 + m] ||
-          (m == 2 && p[8 + m] == f[8 + m] && p[16] >= 0 && (f[16] < 0 || p[16] < f[16]))) {
-        f[8 + m] = p[8 + m];
-        if (m == 2) f[16] = p[16];
-      }
-      if (p[12 + m] < f[12 + m] ||
-          (m == 2 && p[12 + m] == f[12 + m] && p[17] >= 0 && (f[17] < 0 || p[17] < f[17]))) {
-        f[12 + m] = p[12 + m];
-        if (m == 2) f[17] = p[17];
-      }
-    }
-    f[18] += p[18];
+  for (int64_t t = d + (int64_t)D * i; t < nthreads; t += (int64_t)D * kFeatRed) {
+    double p[kFeat];
+    for (int q = 0; q < kFeat; ++q) p[q] = part[t * kFeat + q];
+    feat_merge(f, p);
   }
-  for (int i = 0; i < kFeat; ++i) feat[(int64_t)d * kFeat + i] = f[i];
+  for (int q = 0; q < kFeat; ++q) sh[i * kFeat + q] = f[q];
+  __syncthreads();
+  for (int h = kFeatRed / 2; h > 0; h >>= 1) {
+    if (i < h) {
+      for (int q = 0; q < kFeat; ++q) f[q] = sh[i * kFeat + q];
+      feat_merge(f, sh + (i + h) * kFeat);
+      for (int q = 0; q < kFeat; ++q) sh[i * kFeat + q] = f[q];
+    }
+    __syncthreads();
+  }
+  if (i < kFeat) feat[(int64_t)d * kFeat + i] = sh[i];
 }
 
 int sm_count() {
@@ -521,7 +542,10 @@ extern "C" int hoi_features(const double *out, int64_t rows, int32_t D, int64_t 
   cudaStream_t s = (cudaStream_t)stream;
   int bs = (256 / D) * D;                      // a multiple of D: one dataset per thread
   if (bs < D) bs = D;
-  int blocks = 4 * sm_count();
+  // grid sized by the work (>= 32 units per thread), at most 4 CTAs per SM:
+  // small chunks must not write and re-read a full grid of partials
+  const int64_t want = (rows * (int64_t)D + (int64_t)bs * 32 - 1) / ((int64_t)bs * 32);
+  int blocks = (int)(want < 4 * sm_count() ? (want > 0 ? want : 1) : 4 * sm_count());
   if ((int64_t)blocks * bs * kFeat > ws_doubles) blocks = (int)(ws_doubles / ((int64_t)bs * kFeat));
   if (blocks < 1) return fail(HOI_CAPACITY, "hoi_features: workspace too small");
   const int64_t nthreads = (int64_t)blocks * bs;
@@ -529,7 +553,7 @@ extern "C" int hoi_features(const double *out, int64_t rows, int32_t D, int64_t 
                                            pair_end, reinterpret_cast<double *>(ws));
   int st = check_launch("k_features_partial");
   if (st) return st;
-  k_features_reduce<<<(D + 63) / 64, 64, 0, s>>>(reinterpret_cast<double *>(ws), nthreads, D, feat);
+  k_features_reduce<<<D, kFeatRed, 0, s>>>(reinterpret_cast<double *>(ws), nthreads, D, feat);
   return check_launch("k_features_reduce");
 }
 
