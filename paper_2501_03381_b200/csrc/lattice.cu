@@ -487,6 +487,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// A consumer thread's shared-memory reads of a ring slot must be complete
+// before the slot is handed back to the producer, whose next TMA write
+// (async proxy) would otherwise overtake loads still in flight -- observed
+// on B200 as the first entries of a neighbour slot holding the NEXT job's
+// data once consumers fell behind (multi-dataset scans, slow strided output
+// stores).  Every consumer thread orders its generic-proxy accesses before
+// the async proxy, then the warp releases the slot.
+__device__ __forceinline__ void release_slot(uint64_t *empty_bar, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
+}
+
 constexpr unsigned kEndBlock = 0xFFFFFFFFu;
 constexpr int kBlkQ = 16;              // > blocks the producer can run ahead (kRing + 1)
 
@@ -540,7 +553,7 @@ struct StencilPass {
   const unsigned *list;
   const unsigned *nlist;
   int prefetch;       // claim-ahead L2 prefetch of the own / pass-1-sum blocks
-  unsigned nstack;    // > 1: a stack of that many datasets' tables (see claim())
+  unsigned nstack;    // > 0: a stack of that many datasets' tables (see claim())
 };
 
 // Compact the flagged blocks into a list in claim order (natural, or
@@ -671,7 +684,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       for (;;) {
         const unsigned c = atomicAdd(counter, 1u);
         if (c >= blk_end - blk_begin) return kEndBlock;
-        if (ps.nstack > 1) {
+        if (ps.nstack > 0) {
           // stacked datasets, claimed 4 datasets per block: output rows are
           // (rows, D) with datasets adjacent, so the 4 writes that fill a
           // 32 B sector arrive together and merge in L2 (dataset-major order
@@ -791,14 +804,12 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
         acc[r].x += v.x;
         acc[r].y += v.y;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[slot]);
+      release_slot(&sm.empty[slot], lane);
     }
     if (!OWN) {
       // low pass: the neighbour sums of P, in the table's (swizzled) layout
       if (nj == 0) {                               // the zero job that carried P
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[J % kRing]);
+        release_slot(&sm.empty[J % kRing], lane);
         ++J;
       }
       double *dst = ps.sums + (int64_t)Pg * BLK;
@@ -887,8 +898,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);  // own slot free
+    release_slot(&sm.empty[slot], lane);          // own slot free
     if (NB == 1) named_bar_sync(1, kStencilThreads);   // nbs free for the next block
     ++J;
   }

@@ -442,6 +442,47 @@ def test_lattice_multi_dataset(oracle):
     np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
 
 
+def test_lattice_dataset_stacks(oracle):
+    """Multi-dataset lattice scans below N = 24 run as stacks (one table
+    launch and one stencil launch per stack, claimed 4 datasets per block):
+    D = 9 with per-dataset bias rows vs the oracle; D = 65 at N = 20 (two
+    stacks of the 512 MB table budget) vs the per-n-plet engine."""
+    sigs = np.stack([_random_cov(14, 40 + s) for s in range(9)])
+    sigs = 0.5 * (sigs + sigs.transpose(0, 2, 1))
+    ts = [200 + 17 * s for s in range(9)]
+    covs = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=t) for s, t in zip(sigs, ts)])
+    dev = hoi.scan_device(covs, 2, 14, bias_correct=True, engine=2)
+    _, vals = oracle.scan(sigs, ts, 2, 14, oracle.CollectR(), bias=True)
+    np.testing.assert_allclose(dev.out.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
+    # shrunk towards I: a raw randcorr(20) can be so ill-conditioned at
+    # order 20 that any two elimination orders differ beyond 1e-9
+    big = hoi.CovSet([hoi.CovarianceMatrix(
+        0.6 * workloads.randcorr(20, np.random.default_rng(s)) + 0.4 * np.eye(20),
+        n_samples_used=500 + s) for s in range(65)])
+    a = hoi.scan_device(big, 2, 20, bias_correct=True, engine=2).out
+    b = hoi.scan_device(big, 2, 20, bias_correct=True, engine=1).out
+    err = (a - b).abs() - 1e-9 * b.abs()
+    assert float(err.max()) <= 1e-11
+    assert bool((a[3] == a[0] + a[1]).all())
+    del a, b
+    torch.cuda.empty_cache()
+
+
+def test_lattice_scans_are_deterministic():
+    """Repeated multi-dataset lattice scans are bit-identical.  Regression:
+    when consumers lagged (D >= 4, strided output stores) a ring slot could
+    be refilled by TMA while shared loads of it were still in flight (fixed
+    with a proxy fence before each slot release)."""
+    for n, d in ((20, 8), (22, 4)):
+        covs = hoi.CovSet([hoi.CovarianceMatrix(workloads.randcorr(n, np.random.default_rng(s)))
+                           for s in range(d)])
+        ref = hoi.scan_device(covs, 2, n, engine=2).out
+        for _ in range(3):
+            assert bool((hoi.scan_device(covs, 2, n, engine=2).out == ref).all())
+        del ref
+        torch.cuda.empty_cache()
+
+
 def test_lattice_declines_singular_covariance(oracle):
     """A duplicated variable makes R singular: the lattice engine declines
     and the per-n-plet engine applies the reference's jitter rule."""
