@@ -225,6 +225,10 @@ def _indices_to_device(indices, torch):
     copy -- numpy's single-threaded astype plus a pageable copy cost ~55 ms
     for BASELINE config 5's 4M x 10 indices."""
     src = torch.from_numpy(np.ascontiguousarray(indices))
+    if src.numel() * 4 > (256 << 20):
+        # very large batches: no multi-GB pinned block held by torch's
+        # caching host allocator; still a multi-threaded conversion
+        return src.to(torch.int32).cuda()
     host = torch.empty(src.shape, dtype=torch.int32, pin_memory=True)
     host.copy_(src)
     return host.to("cuda", non_blocking=True)
