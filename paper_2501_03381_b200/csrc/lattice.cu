@@ -92,6 +92,7 @@ __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
 // serialises divergent indices; these go through L1 with coalescing).
 __device__ uint16_t g_runmask[BLK];
 __device__ uint32_t g_run[BLK];          // run position p -> e | lexrank << 10 | q << 20
+__device__ uint16_t g_lexrank[BLK];      // Q mask -> rank among |Q|-subsets (filter epilogue)
 __device__ uint64_t g_binom[kBinomN * kBinomN];
 
 __device__ __forceinline__ uint64_t binom_g(int n, int m) {
@@ -352,6 +353,8 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+constexpr uint32_t kSuspendHintNs = 20000;   // upper bound on one suspension
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
@@ -361,14 +364,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing the probe.  Without
+// it the probe loops were ~1/3 of the instructions the filtered stencil
+// issued (ncu source view); with it they are gone from the top lines, but
+// the kernel time did not move (10.18 ms either way): the waits are real
+// data waits, the probes only filled idle issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(bar)), "r"(phase), "r"(kSuspendHintNs)
         : "memory");
   }
 }
@@ -823,6 +832,87 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     const int slot = J % kRing;
     mbar_wait(&sm.full[slot], (J / kRing) & 1u);
     const double *own = sm.ring[slot];
+    if (FILTER) {
+      // Filter mode writes no ordered output, so each thread finishes its own
+      // entry pairs from registers and the own slot goes back to the producer
+      // BEFORE the epilogue: the ring (4 slots, ~7 jobs per block) can then
+      // hold the next block's loads while this block's measures are filtered,
+      // instead of exposing their latency after it.  Rows: base[q] + lexrank.
+      double lv[PAIRS][2], nv[PAIRS][2];
+#pragma unroll
+      for (int r = 0; r < PAIRS; ++r) {
+        const int e0 = 2 * (tid + kStencilThreads * r);
+        const double2 ov = *reinterpret_cast<const double2 *>(own + pw[r]);
+        const double o0 = flip[r] ? ov.y : ov.x, o1 = flip[r] ? ov.x : ov.y;
+        double s0 = flip[r] ? acc[r].y : acc[r].x;
+        double s1 = (flip[r] ? acc[r].x : acc[r].y) + o0;   // bit-0 neighbour of e0+1 is e0
+#pragma unroll
+        for (int t = 1; t < CB; ++t) {
+          if ((e0 >> t) & 1) {
+            const int n0 = e0 ^ (1 << t);
+            const double2 v = *reinterpret_cast<const double2 *>(own + (swz(n0) & ~1));
+            const bool f = (n0 >> 5) & 1;
+            s0 += f ? v.y : v.x;
+            s1 += f ? v.x : v.y;
+          }
+        }
+        lv[r][0] = o0;
+        lv[r][1] = o1;
+        nv[r][0] = s0;
+        nv[r][1] = s1;
+      }
+      release_slot(&sm.empty[slot], lane);          // own slot free before the epilogue
+      named_bar_sync(1, kStencilThreads);           // base[buf] complete
+#pragma unroll
+      for (int r = 0; r < PAIRS; ++r) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = 2 * (tid + kStencilThreads * r) + h;
+          const int q = __popc(e);
+          const int64_t b0 = sm.base[buf][q];
+          const int k = kP + q;
+          const int64_t row = b0 + (int64_t)__ldg(g_lexrank + e);
+          const bool valid = b0 != kNoRun && row >= 0 && row < rows;
+          double tc = 0.0, dtc = 0.0, o = 0.0;
+          if (valid) {
+            const double l = lv[r][h], nb = nv[r][h];
+            const double kd = (double)k;
+            if (et) {
+              const double ek = et[k], ek1 = et[k - 1];
+              tc = -0.5 * l - kd * e1 + ek;
+              dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
+              o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+            } else {
+              tc = -0.5 * l;
+              dtc = 0.5 * ((1.0 - kd) * l + nb);
+              o = 0.5 * ((kd - 2.0) * l - nb);
+            }
+          }
+          const double sv = tc + dtc;
+          const double v = flt.m_idx == 0 ? tc : flt.m_idx == 1 ? dtc : flt.m_idx == 2 ? o : sv;
+          const bool keep = valid && orderable_key(flt.sign * v) <= key_max;
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (bal) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(flt.count, (unsigned long long)__popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (keep) {
+              const unsigned long long slot2 = base + __popc(bal & ((1u << lane) - 1u));
+              if ((int64_t)slot2 < flt.cap) {
+                double *rec = flt.cand + 5 * slot2;
+                rec[0] = __longlong_as_double(row + g_begin);
+                rec[1] = tc;
+                rec[2] = dtc;
+                rec[3] = o;
+                rec[4] = sv;
+              }
+            }
+          }
+        }
+      }
+      ++J;
+      continue;
+    }
     double *nbs = sm.nbs[NB == 2 ? buf : 0];
 #pragma unroll
     for (int r = 0; r < PAIRS; ++r) {
@@ -1175,6 +1265,7 @@ void upload_tables() {
     cudaMemcpyToSymbol(g_binom, hb.data(), sizeof(uint64_t) * hb.size());
   }
   cudaMemcpyToSymbol(c_lexrank, lr.data(), sizeof(uint16_t) * BLK);
+  cudaMemcpyToSymbol(g_lexrank, lr.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runmask, rm.data(), sizeof(uint16_t) * BLK);
   cudaMemcpyToSymbol(c_runstart, rs.data(), sizeof(uint16_t) * (CB + 2));
   {
