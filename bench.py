@@ -254,37 +254,40 @@ def lattice_roofline(torch, lib, nat, ctx, out, g0, g1, step_ms, steps):
             "kernel_share_of_step": (tm + tt) / step_ms}
 
 
-def shard_roofline(torch, nat, ctx, out, rank, sb, step_ms, steps):
+def shard_roofline(torch, nat, ctx, out, rank, sb, mask, step_ms, steps):
     """N > 1 (block shards): CUDA-event timing of this rank's whole shard
-    step (hoi_lattice_shard: its 1 + popc(rank) table chunks, then the
+    step (hoi_lattice_shard_set: the table chunks its shards read, then the
     stencil over its own blocks), gathered from every rank; the slowest
-    rank is reported.  Algorithmic bytes of rank r: the table chunks it
+    rank is reported.  Algorithmic bytes of a rank: the table chunks it
     writes and reads back (8 B x 2^(N-sb) each) + 32 B per n-plet it owns
-    (patterns of popcount p over the sb shard variables:
-    sum_k C(N - sb, k - p) rows)."""
+    (shard c, popcount p: sum_k C(N - sb, k - p) rows)."""
     import torch.distributed as dist
-    from paper_2501_03381_b200.sharding import allgather_objects
+    from paper_2501_03381_b200.sharding import allgather_objects, shard_set_chunks
     ts = []
     for _ in range(steps):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
-        ctx.full_shard(rank, sb, out)
+        ctx.full_shard_set(mask, sb, out)
         ev[1].record()
         torch.cuda.synchronize()
         ts.append(ev[0].elapsed_time(ev[1]))
     t = float(np.mean(ts))
-    p = bin(rank).count("1")
     chunk = 8 * (1 << (N - sb))
-    rows = sum(math.comb(N - sb, k - p) for k in range(LO, HI + 1) if 0 <= k - p <= N - sb)
-    alg = 2 * (1 + p) * chunk + 32 * rows
-    per = allgather_objects((t, alg, rank, rows))
-    t, alg, r, rows = max(per)
+    nchunks = len(shard_set_chunks(mask, sb))
+    rows = 0
+    for c in range(1 << sb):
+        if (mask >> c) & 1:
+            p = bin(c).count("1")
+            rows += sum(math.comb(N - sb, k - p) for k in range(LO, HI + 1) if 0 <= k - p <= N - sb)
+    alg = 2 * nchunks * chunk + 32 * rows
+    per = allgather_objects((t, alg, rank, rows, nchunks))
+    t, alg, r, rows, nchunks = max(per)
     peak, src = measured_peaks()
     achieved = alg / (t * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": None,
-            "kernel": f"hoi_lattice_shard of the slowest rank ({r} of {dist.get_world_size()}): "
-                      "its table chunks (k_lattice_table) + its stencil share "
+            "kernel": f"hoi_lattice_shard_set of the slowest rank ({r} of {dist.get_world_size()}): "
+                      f"its {nchunks} table chunks of 2^{sb} (k_lattice_table) + its stencil share "
                       "(k_lattice_measures)",
             "peak_source": src, "algorithmic_bytes_per_launch": alg,
             "algorithmic_bytes_note": "table chunks written and read once (8 B x 2^(N-sb) "
@@ -490,22 +493,24 @@ def b200_arm(a):
     import paper_2501_03381_b200 as hoi
     from paper_2501_03381_b200 import _build, _native as nat, workloads
     from paper_2501_03381_b200.scanner import _ScanCtx
-    from paper_2501_03381_b200.sharding import block_shard_bits, nplet_flops, rank_ranges
+    from paper_2501_03381_b200.sharding import block_shard_plan, nplet_flops, rank_ranges
     _build.build()
     lib = nat.load()
 
     x = workloads.cfg4()
     covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
     ctx = _ScanCtx(covs, LO, HI, False, a.engine)
-    sb = block_shard_bits(N, world) if world > 1 and ctx.engine == 2 else None
-    if sb is not None:
-        # block shards: this rank's n-plets at their global rows of a
-        # full-size output (rows of other ranks untouched)
+    plan = block_shard_plan(N, world) if world > 1 and ctx.engine == 2 else None
+    sb = plan[0] if plan else None
+    if plan is not None:
+        # block shards: this rank's shard pair (r, 2^sb-1-r), its n-plets at
+        # their global rows of a full-size output (rows of other ranks untouched)
         g0, g1 = 0, TOTAL
         out = torch.empty((4, TOTAL, 1), dtype=torch.float64, device="cuda")
+        mask = plan[1][rank]
 
         def step():
-            ctx.full_shard(rank, sb, out)
+            ctx.full_shard_set(mask, sb, out)
     else:
         g0, g1 = rank_ranges(N, LO, HI, world, "count" if a.engine != 1 else "flops")[rank]
         out = torch.empty((4, g1 - g0, 1), dtype=torch.float64, device="cuda")
@@ -543,8 +548,8 @@ def b200_arm(a):
         roof = lattice_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
     if rank == 0 and engine_used == 3:
         roof = fused_roofline(torch, lib, nat, ctx, out, g0, g1, ms, a.steps)
-    if sb is not None:
-        roof = shard_roofline(torch, nat, ctx, out, rank, sb, ms, a.steps)
+    if plan is not None:
+        roof = shard_roofline(torch, nat, ctx, out, rank, sb, plan[1][rank], ms, a.steps)
     del out
     torch.cuda.empty_cache()
     fp64 = None
@@ -564,7 +569,8 @@ def b200_arm(a):
                                    "full output (4 x f64 per n-plet) written to HBM",
                        "nplets": TOTAL, "engine": engine_used,
                        "l2_flush": "each step writes 34.4 GB of output (> 126 MB L2)",
-                       "parallelism": (f"lattice block shards x{world} (top {sb} prefix bits)"
+                       "parallelism": (f"lattice block shards x{world} (top {sb} prefix bits, "
+                                        f"{bin(plan[1][0]).count('1')} shards per rank)"
                                        if sb is not None else f"rank-range shards x{world}")},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -228,6 +228,20 @@ int hoi_lattice_shard_filter(const double *corr, int32_t N, int32_t D, int32_t d
                              double sign, const uint64_t *key_max, double *cand,
                              int64_t cand_cap, uint64_t *count, int32_t build_table, void *ws,
                              size_t ws_bytes, void *stream);
+/* hoi_lattice_shard_set / _set_filter: several shards on one GPU, bit c of
+ * shard_mask = shard c of 2^shard_bits (shard_bits <= 6); each needed table
+ * chunk is built once.  Owning complementary shards (c and 2^shard_bits-1-c)
+ * balances the rebuild work across GPUs (sharding.block_shard_plan). */
+int hoi_lattice_shard_set(const double *corr, int32_t N, int32_t D, int32_t d, const double *eta,
+                          int32_t kstride, int32_t kmin, int32_t kmax, uint64_t shard_mask,
+                          int32_t shard_bits, double *out, void *ws, size_t ws_bytes,
+                          void *stream);
+int hoi_lattice_shard_set_filter(const double *corr, int32_t N, int32_t D, int32_t d,
+                                 const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
+                                 uint64_t shard_mask, int32_t shard_bits, int32_t every,
+                                 int32_t m_idx, double sign, const uint64_t *key_max,
+                                 double *cand, int64_t cand_cap, uint64_t *count,
+                                 int32_t build_table, void *ws, size_t ws_bytes, void *stream);
 
 /* Engine 3: both phases in ONE persistent pass (dataset d).  Warps claim
  * table blocks in increasing order, build and publish their block, then

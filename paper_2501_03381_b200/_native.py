@@ -52,6 +52,11 @@ _SIGS = {
                            _sz, _vp], C.c_int),
     "hoi_lattice_shard_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                   _i32, _dbl, _vp, _vp, _i64, _vp, _i32, _vp, _sz, _vp], C.c_int),
+    "hoi_lattice_shard_set": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, C.c_uint64, _i32,
+                               _vp, _vp, _sz, _vp], C.c_int),
+    "hoi_lattice_shard_set_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, C.c_uint64,
+                                      _i32, _i32, _i32, _dbl, _vp, _vp, _i64, _vp, _i32, _vp, _sz,
+                                      _vp], C.c_int),
     "hoi_lattice_filter": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _dbl, _i32, _vp,
                             _vp, _i64, _vp, _vp], C.c_int),
     "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,

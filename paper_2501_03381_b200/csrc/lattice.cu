@@ -465,13 +465,14 @@ __global__ void k_block_sample(unsigned nblocks, unsigned every, uint8_t *__rest
   }
 }
 
-// Block shard `shard` of 2^sb: the table blocks whose top sb prefix bits
-// equal shard (optionally intersected with a hash sample, every > 1).
-__global__ void k_block_shard(unsigned nblocks, int nP, int sb, unsigned shard, unsigned every,
-                              uint8_t *__restrict__ active) {
+// Block shards `mask` of 2^sb: the table blocks whose top sb prefix bits
+// name a shard in the mask (optionally intersected with a hash sample,
+// every > 1).
+__global__ void k_block_shard(unsigned nblocks, int nP, int sb, unsigned long long mask,
+                              unsigned every, uint8_t *__restrict__ active) {
   const unsigned P = blockIdx.x * blockDim.x + threadIdx.x;
   if (P >= nblocks) return;
-  bool on = sb == 0 || (P >> (nP - sb)) == shard;
+  bool on = sb == 0 || ((mask >> (P >> (nP - sb))) & 1ull);
   if (every > 1) on = on && (((uint64_t)(P * 2654435761u) * every) >> 32) == 0;
   active[P] = on ? 1 : 0;
 }
@@ -1610,17 +1611,23 @@ int lattice_filter(void *ws, int N, int D, int d, const double *eta, int kstride
 // sample of the shard's blocks).
 int lattice_status(void *ws, int N, cudaStream_t s);
 
+// Block shards `mask` (bit c = shard c of 2^sb owned by this GPU): build the
+// table chunks their stencil reads -- each owned chunk and every chunk that
+// differs from one by a single cleared bit, each once -- then stream the
+// owned blocks.  Owning complementary chunks (c and 2^sb - 1 - c) evens out
+// the rebuild work across GPUs (sharding.block_shard_plan).
 int lattice_shard(const double *corr, int N, int D, int d, const double *eta, int kstride,
-                  int kmin, int kmax, int shard, int sb, unsigned every, double *out,
-                  const StencilFilter *flt, bool build, void *ws, size_t ws_bytes,
+                  int kmin, int kmax, unsigned long long mask, int sb, unsigned every,
+                  double *out, const StencilFilter *flt, bool build, void *ws, size_t ws_bytes,
                   cudaStream_t s) {
   size_t need = 0;
   int st = lattice_ws_bytes(N, D, &need);
   if (st) return st;
   if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
   const int nP = N - CB;
-  if (sb < 0 || sb > nP / 2 || shard < 0 || shard >= (1 << sb))
-    return fail(HOI_INVALID_ARG, "lattice_shard: need 0 <= shard < 2^sb, sb <= (N-10)/2");
+  if (sb < 0 || sb > nP / 2 || sb > 6 || mask == 0 || (sb < 6 && (mask >> (1 << sb)) != 0))
+    return fail(HOI_INVALID_ARG,
+                "lattice_shard: need a non-empty shard mask below 2^(2^sb), sb <= min(6, (N-10)/2)");
   upload_binomials();
   upload_tables();
   LatticeWs w = ws_view(ws, N);
@@ -1631,15 +1638,17 @@ int lattice_shard(const double *corr, int N, int D, int d, const double *eta, in
   const unsigned chunk_ctas = 1u << (nP - b - sb);     // table CTAs of one shard chunk
   if (build) cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   for (unsigned c = 0; build && c < (1u << sb); ++c) {
-    if ((c & ~(unsigned)shard) != 0) continue;         // c must be shard with some bits cleared
-    if (c != (unsigned)shard && __builtin_popcount((unsigned)shard ^ c) != 1) continue;
+    bool need = false;                                 // c owned, or an owned shard minus one bit
+    for (unsigned o = 0; o < (1u << sb) && !need; ++o)
+      need = ((mask >> o) & 1ull) && (c & ~o) == 0 && __builtin_popcount(o ^ c) <= 1;
+    if (!need) continue;
     k_lattice_table<8><<<chunk_ctas, 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag,
                                                   c * chunk_ctas);
     if ((st = check_launch("k_lattice_table"))) return st;
   }
   if (build && (st = lattice_status(ws, N, s))) return st;
   const unsigned nblocks = 1u << nP;
-  k_block_shard<<<(nblocks + 255) / 256, 256, 0, s>>>(nblocks, nP, sb, (unsigned)shard, every,
+  k_block_shard<<<(nblocks + 255) / 256, 256, 0, s>>>(nblocks, nP, sb, mask, every,
                                                       reinterpret_cast<uint8_t *>(w.ready));
   if ((st = check_launch("k_block_shard"))) return st;
   return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, out, 0u, nblocks,
@@ -1861,7 +1870,21 @@ extern "C" int hoi_lattice_shard(const double *corr, int32_t N, int32_t D, int32
                     kmin <= kmax && kmax <= N,
                 "hoi_lattice_shard: bad args");
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard: bias table too short");
-  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard, shard_bits, 1u, out,
+  HOI_CHECK_ARG(shard_bits >= 0 && shard_bits <= 6 && shard >= 0 && shard < (1 << shard_bits),
+                "hoi_lattice_shard: need 0 <= shard < 2^shard_bits <= 64");
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, 1ull << shard, shard_bits, 1u,
+                       out, nullptr, true, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_shard_set(const double *corr, int32_t N, int32_t D, int32_t d,
+                                     const double *eta, int32_t kstride, int32_t kmin,
+                                     int32_t kmax, uint64_t shard_mask, int32_t shard_bits,
+                                     double *out, void *ws, size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && out && lattice_supports(N) && d >= 0 && d < D && kmin >= 1 &&
+                    kmin <= kmax && kmax <= N,
+                "hoi_lattice_shard_set: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_set: bias table too short");
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard_mask, shard_bits, 1u, out,
                        nullptr, true, ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -1877,9 +1900,31 @@ extern "C" int hoi_lattice_shard_filter(const double *corr, int32_t N, int32_t D
                     every >= 1,
                 "hoi_lattice_shard_filter: bad args");
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_filter: bias table too short");
+  HOI_CHECK_ARG(shard_bits >= 0 && shard_bits <= 6 && shard >= 0 && shard < (1 << shard_bits),
+                "hoi_lattice_shard_filter: need 0 <= shard < 2^shard_bits <= 64");
   StencilFilter f{m_idx, sign, key_max, cand, reinterpret_cast<unsigned long long *>(count),
                   cand_cap};
-  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard, shard_bits,
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, 1ull << shard, shard_bits,
+                       (unsigned)every, nullptr, &f, build_table != 0, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_shard_set_filter(const double *corr, int32_t N, int32_t D, int32_t d,
+                                            const double *eta, int32_t kstride, int32_t kmin,
+                                            int32_t kmax, uint64_t shard_mask,
+                                            int32_t shard_bits, int32_t every, int32_t m_idx,
+                                            double sign, const uint64_t *key_max, double *cand,
+                                            int64_t cand_cap, uint64_t *count,
+                                            int32_t build_table, void *ws, size_t ws_bytes,
+                                            void *stream) {
+  HOI_CHECK_ARG(corr && ws && key_max && cand && count && lattice_supports(N) && d >= 0 &&
+                    d < D && kmin >= 1 && kmin <= kmax && kmax <= N && m_idx >= 0 && m_idx < 4 &&
+                    every >= 1,
+                "hoi_lattice_shard_set_filter: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_set_filter: bias table too short");
+  StencilFilter f{m_idx, sign, key_max, cand, reinterpret_cast<unsigned long long *>(count),
+                  cand_cap};
+  return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard_mask, shard_bits,
                        (unsigned)every, nullptr, &f, build_table != 0, ws, ws_bytes,
                        (cudaStream_t)stream);
 }

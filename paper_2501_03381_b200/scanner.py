@@ -421,6 +421,25 @@ class _ScanCtx:
         return out, cnt, coords
 
 
+    def full_shard_set(self, shard_mask: int, shard_bits: int, out=None):
+        """Lattice engine, the block shards in `shard_mask` (bit c = shard c
+        of 2^shard_bits) on this GPU, each n-plet at its GLOBAL row of a
+        full-size (4, total, D) output (see full_shard)."""
+        torch, lib = self.torch, nat.lib()
+        total = count_nplets(self.n, self.lo, self.hi)
+        if out is None:
+            out = torch.empty((4, total, self.d), dtype=torch.float64, device="cuda")
+        s = nat.stream_handle(torch)
+        kst = 0 if self.eta is None else self.eta.shape[1]
+        for d in range(self.d):
+            nat.check(lib.hoi_lattice_shard_set(self.st.corr.data_ptr(), self.n, self.d, d,
+                                                nat.ptr(self.eta), kst, self.lo, self.hi,
+                                                int(shard_mask), shard_bits, out.data_ptr(),
+                                                self.ws.data_ptr(), self.ws.numel(), s),
+                      "lattice_shard_set")
+        self._table_ok = False
+        return out
+
     def full_shard(self, shard: int, shard_bits: int, out=None):
         """Lattice engine, block shard `shard` of 2^shard_bits: every n-plet
         of the shard's table blocks at its GLOBAL row of a full-size
@@ -438,6 +457,14 @@ class _ScanCtx:
                                             self.ws.numel(), s), "lattice_shard")
         self._table_ok = False
         return out
+
+
+def shard_set_rows(n: int, lo: int, hi: int, shard_mask: int, shard_bits: int) -> np.ndarray:
+    """Global ranks owned by the block shards in `shard_mask` (host model of
+    hoi_lattice_shard_set's partition, for tests)."""
+    parts = [shard_rows(n, lo, hi, c, shard_bits) for c in range(1 << shard_bits)
+             if (shard_mask >> c) & 1]
+    return np.sort(np.concatenate(parts)) if parts else np.zeros(0, dtype=np.int64)
 
 
 def shard_rows(n: int, lo: int, hi: int, shard: int, shard_bits: int) -> np.ndarray:
@@ -688,7 +715,7 @@ def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
 
 
 @_gc_paused
-def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
+def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0, shard_mask=None):
     """TopK over an exhaustive scan without writing the full output (lattice
     engine): per dataset, (1) build the log-det table; (2) run the filtered
     stencil over every 256th table block with no threshold and take the
@@ -700,7 +727,9 @@ def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
     the reference's host merge (sign*value, index tuple).  Returns False
     when the engine declines (not PD) or the sample is smaller than k; the
     caller then takes the full-output path.  shard_bits > 0: only the
-    n-plets of block shard `shard` (multi-GPU; see ScanCtx.full_shard)."""
+    n-plets of block shard `shard`, or of the shards in `shard_mask`
+    (multi-GPU; see ScanCtx.full_shard_set)."""
+    mask = (1 << shard) if shard_mask is None else int(shard_mask)
     torch, lib = ctx.torch, nat.lib()
     s = nat.stream_handle(torch)
     n = ctx.n
@@ -731,9 +760,9 @@ def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0):
                                             ctx.lo, ctx.hi, m_idx, sign, every_, key.data_ptr(),
                                             cand.data_ptr(), cap, cnt.data_ptr(), s)
             else:
-                rc = lib.hoi_lattice_shard_filter(
+                rc = lib.hoi_lattice_shard_set_filter(
                     ctx.st.corr.data_ptr(), n, ctx.d, d, nat.ptr(ctx.eta), kst, ctx.lo, ctx.hi,
-                    shard, shard_bits, every_, m_idx, sign, key.data_ptr(), cand.data_ptr(), cap,
+                    mask, shard_bits, every_, m_idx, sign, key.data_ptr(), cand.data_ptr(), cap,
                     cnt.data_ptr(), 0 if built[0] else 1, ctx.ws.data_ptr(), ctx.ws.numel(), s)
                 if rc == nat.FALLBACK:
                     return None, -1

@@ -1,6 +1,7 @@
-"""Per-rank block-shard step times for G = 2, 4, 8 GPUs, measured one rank at
-a time on ONE B200 (each rank's own work: its 1 + popc(rank) table chunks and
-its stencil share, CUDA events).  The multi-GPU step is bounded below by the
+"""Per-rank block-shard step times for G = 2, 4, 8 GPUs (block_shard_plan:
+two complementary shards per rank), measured one rank at a time on ONE B200
+(each rank's own work: the table chunks its shards read and its stencil
+share, CUDA events).  The multi-GPU step is bounded below by the
 slowest rank; this is that bound, not a concurrent multi-GPU measurement."""
 import json, sys
 from pathlib import Path
@@ -9,7 +10,7 @@ import torch
 import paper_2501_03381_b200 as hoi
 from paper_2501_03381_b200 import _build, workloads
 from paper_2501_03381_b200.scanner import _ScanCtx
-from paper_2501_03381_b200.sharding import block_shard_bits
+from paper_2501_03381_b200.sharding import block_shard_plan
 
 _build.build()
 N, LO, HI = 30, 2, 30
@@ -28,14 +29,14 @@ e1.record(); torch.cuda.synchronize()
 one = e0.elapsed_time(e1) / 3
 res["1"] = {"step_ms": round(one, 3)}
 for g in (2, 4, 8):
-    sb = block_shard_bits(N, g)
+    sb, masks = block_shard_plan(N, g)
     per = []
     for r in range(g):
-        ctx.full_shard(r, sb, out)
+        ctx.full_shard_set(masks[r], sb, out)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(3):
-            ctx.full_shard(r, sb, out)
+            ctx.full_shard_set(masks[r], sb, out)
         e1.record(); torch.cuda.synchronize()
         per.append(round(e0.elapsed_time(e1) / 3, 3))
     res[str(g)] = {"per_rank_ms": per, "max_ms": max(per),

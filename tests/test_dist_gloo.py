@@ -144,3 +144,24 @@ def test_two_rank_topk_and_histogram_merge(oracle, mode):
     np.testing.assert_allclose([e[1] for e in got_top], [w[1] for w in want], rtol=1e-12)
     _, c = oracle.scan(sig, [0], 2, 8, oracle.HistR("tc", 6, -0.2, 1.0))
     assert got_counts == c.tolist()
+
+
+def test_block_shard_plan_partitions_and_balances():
+    """The per-rank shard sets of block_shard_plan partition the rank space,
+    and every rank rebuilds the same number of table chunks at 4 and 8 GPUs."""
+    from paper_2501_03381_b200.scanner import shard_set_rows
+    n, lo, hi = 16, 2, 9
+    total = sum(math.comb(n, k) for k in range(lo, hi + 1))
+    for world in (2, 4, 8):
+        sb, masks = sharding.block_shard_plan(n, world)
+        rows = [shard_set_rows(n, lo, hi, m, sb) for m in masks]
+        allr = np.concatenate(rows)
+        assert len(allr) == total and len(np.unique(allr)) == total
+        if world == 4:    # (at N = 16, 8 ranks need 4 > (N-10)/2 shard bits: one shard each)
+            assert len({len(sharding.shard_set_chunks(m, sb)) for m in masks}) == 1
+    for world in (4, 8):  # the headline N = 30: every rank rebuilds the same number of chunks
+        sb, masks = sharding.block_shard_plan(30, world)
+        assert sb == world.bit_length() and len({len(sharding.shard_set_chunks(m, sb))
+                                                for m in masks}) == 1
+    assert sharding.block_shard_plan(12, 2) == (1, [1, 2])
+

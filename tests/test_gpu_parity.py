@@ -568,6 +568,53 @@ def test_block_shards_reassemble_the_scan(shard_bits):
     assert [e.indices for _, e in merged[0]] == [e.indices for e in single]
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_block_shard_sets_reassemble_the_scan(world):
+    """block_shard_plan's per-rank shard pairs, run one after another on one
+    GPU: each rank's set writes exactly the rows of its shards, the union is
+    bit-identical to the single-GPU scan, and the merged per-rank TopK
+    lists equal the single-GPU TopK."""
+    from paper_2501_03381_b200 import scanner, sharding
+    rng = np.random.default_rng(11)
+    c = workloads.randcorr(22, rng)
+    x = rng.standard_normal((2000, 22)) @ np.linalg.cholesky(c).T
+    covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x))])
+    total = hoi.count_nplets(22, 2, 22)
+    ctx = scanner._ScanCtx(covs, 2, 22, False, 2)
+    want, _, _ = ctx.full(0, total)
+    want = want.clone()
+    sb, masks = sharding.block_shard_plan(22, world)
+    got = torch.full((4, total, 1), float("nan"), dtype=torch.float64, device="cuda")
+    idx, _ = unrank_device(22, 2, 22, 0, total)
+    lo_var = 22 - 10 - sb
+    pat = torch.zeros(total, dtype=torch.int64, device="cuda")
+    for t in range(sb):
+        pat |= (idx == lo_var + t).any(dim=1).long() << t
+    del idx
+    for m in masks:
+        before = torch.isnan(got[0, :, 0])
+        ctx.full_shard_set(m, sb, got)
+        newly = before & ~torch.isnan(got[0, :, 0])
+        own = torch.zeros_like(newly)
+        for cidx in range(1 << sb):
+            if (m >> cidx) & 1:
+                own |= pat == cidx
+        assert torch.equal(newly, own)
+    assert torch.equal(got, want)
+    parts = []
+    for m in masks:
+        red = hoi.TopK("o", "min", 50)
+        assert scanner._topk_lattice(scanner._ScanCtx(covs, 2, 22, False, 2), red, 2,
+                                     shard_bits=sb, shard_mask=m)
+        parts.append(red._best)
+    merged = sharding.merge_topk(parts, 50)
+    one = hoi.scan(covs, 2, 22, hoi.TopK("o", "min", 50))
+    assert [[e.indices for _, e in per] for per in merged] == [[e.indices for e in per]
+                                                               for per in one]
+    del got, want
+    torch.cuda.empty_cache()
+
+
 def test_topk_batch_matches_host_reducer():
     """Device batched TopK == the reference's TopK.update on the same
     HoiBatch (cfg5-style: 16 datasets, N = 400, order-10 random n-plets)."""
