@@ -61,7 +61,7 @@ constexpr int kMinNearBits = 12;
 //                           chunked two-stream table/stencil pipeline
 struct LatticeTuning {
   int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
-  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3;
+  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1;
   LatticeTuning() {
     auto get = [](const char *name, int &v) {
       if (const char *e = getenv(name)) v = atoi(e);
@@ -76,6 +76,7 @@ struct LatticeTuning {
     get("HOI_PIPE_WB", pipe_wb);
     get("HOI_TABLE_NW", table_nw);
     get("HOI_STENCIL_PER_SM", stencil_per_sm);
+    get("HOI_FILTER_RING6", filter_ring6);
   }
 };
 
@@ -415,10 +416,11 @@ constexpr int PER = BLK / kStencilThreads;
 // kNbs = 1: one neighbour-sum buffer (a second consumer barrier per block,
 // 12 KB less shared memory per CTA -> one more ring slot at 4 CTAs/SM; the
 // run table is then read from the global copy g_run through L1).
+// kNbs = 0 (filter mode only): entries finish from registers, no buffer.
 template <int kRing, int kNbs = 2>
 struct StencilSmem {
   double ring[kRing][BLK];           // TMA destination ring
-  double nbs[kNbs][BLK];             // sum of the k leave-one-out log-dets per entry
+  double nbs[kNbs > 0 ? kNbs : 1][kNbs > 0 ? BLK : 1];   // leave-one-out log-det sums per entry
   uint32_t run[kNbs == 2 ? BLK : 1]; // run position p -> e | lexrank << 10 | q << 20
   uint64_t full[kRing];              // TMA landed
   uint64_t empty[kRing];             // every consumer warp is done with the slot
@@ -1541,6 +1543,12 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
                      listed ? cnts + 1 : nullptr, pf};
   }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+  // Filter mode finishes entries from registers (no neighbour-sum buffer),
+  // so 6 ring slots fit at 4 CTAs/SM: 24 TMA jobs in flight per SM, not 16.
+  if (flt && tuning().filter_ring6)
+    return run_stencil<6, 4, MODE_FILTER, 0>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
+                                             g_end, out, plane, blk_begin, blk_end, active,
+                                             near_bits, own_last, per_sm_cap, *flt, ps, s);
   if (flt && ring == 5)
     return run_stencil<5, 4, MODE_FILTER, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
                                              g_end, out, plane, blk_begin, blk_end, active,
