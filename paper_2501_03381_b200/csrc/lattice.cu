@@ -61,7 +61,7 @@ constexpr int kMinNearBits = 12;
 //                           chunked two-stream table/stencil pipeline
 struct LatticeTuning {
   int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
-  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1;
+  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1, lowsum_ring6 = 1;
   LatticeTuning() {
     auto get = [](const char *name, int &v) {
       if (const char *e = getenv(name)) v = atoi(e);
@@ -77,6 +77,7 @@ struct LatticeTuning {
     get("HOI_TABLE_NW", table_nw);
     get("HOI_STENCIL_PER_SM", stencil_per_sm);
     get("HOI_FILTER_RING6", filter_ring6);
+    get("HOI_LOWSUM_RING6", lowsum_ring6);
   }
 };
 
@@ -1531,7 +1532,13 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   if (two) {
     StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0};
     cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
-    int st = ring == 5
+    // the low pass stores its sums straight from registers: no neighbour-sum
+    // buffer or run table, so 6 ring slots fit at 4 CTAs/SM
+    int st = tuning().lowsum_ring6
+                 ? run_stencil<6, 4, MODE_LOWSUM, 0>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
+                                                     g_end, out, plane, blk_begin, blk_end, active,
+                                                     near_bits, own_last, per_sm_cap, none, p1, s)
+             : ring == 5
                  ? run_stencil<5, 4, MODE_LOWSUM, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
                                                      g_end, out, plane, blk_begin, blk_end, active,
                                                      near_bits, own_last, per_sm_cap, none, p1, s)
