@@ -283,6 +283,11 @@ int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign,
  * workspace of at least 4096 uint64. */
 int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
                        int64_t k, uint64_t *key_out, void *ws, void *stream);
+/* hoi_topk_bound: an upper bound of that key -- the end of its bucket after
+ * resolving its top `bits` bits (12 per synchronous radix round); bits >= 64
+ * gives the exact key.  The lattice TopK threshold uses 36 bits. */
+int hoi_topk_bound(const double *vals, int64_t n, int32_t D, int32_t d, double sign, int64_t k,
+                   int32_t bits, uint64_t *key_out, void *ws, void *stream);
 
 /* Candidate filter for TopK: writes the positions p in [0, n) of plane
  * `vals` (stride D, dataset d) whose key sign*vals[p*D+d] <= *thresh into

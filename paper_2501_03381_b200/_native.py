@@ -70,6 +70,7 @@ _SIGS = {
     "hoi_features": ([_vp, _i64, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_objective": ([_vp, _i64, _i32, _i32, _vp, _vp, _i32, _dbl, _vp, _vp, _vp], C.c_int),
     "hoi_topk_threshold": ([_vp, _i64, _i32, _i32, _dbl, _i64, _vp, _vp, _vp], C.c_int),
+    "hoi_topk_bound": ([_vp, _i64, _i32, _i32, _dbl, _i64, _i32, _vp, _vp, _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_histogram": ([_vp, _i64, _i32, _i32, _dbl, _dbl, _vp, _vp, _vp], C.c_int),
     "hoi_fp64_probe": ([_vp, _i64, _i32, _vp], C.c_int),

@@ -478,11 +478,28 @@ extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, d
 // The exact k-th smallest orderable key of sign*vals[p*D+d], p < n (full
 // 64-bit radix select), written to device memory *key_out; ~0 when n <= k
 // (every element qualifies).  Synchronous.
+static int topk_key(const double *vals, int64_t n, int32_t D, int32_t d, double sign, int64_t k,
+                    int bits_wanted, uint64_t *key_out, void *ws, cudaStream_t s);
+
 extern "C" int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
                                   int64_t k, uint64_t *key_out, void *ws, void *stream) {
   HOI_CHECK_ARG(vals && key_out && ws && d >= 0 && d < D && k >= 1 && n >= 0,
                 "hoi_topk_threshold: bad args");
-  cudaStream_t s = (cudaStream_t)stream;
+  return topk_key(vals, n, D, d, sign, k, 64, key_out, ws, (cudaStream_t)stream);
+}
+
+// An upper bound of that key after resolving only its top `bits` bits (the
+// end of the k-th key's bucket): enough for a filter threshold, with fewer
+// synchronous radix rounds (12 bits each).  bits >= 64 is the exact key.
+extern "C" int hoi_topk_bound(const double *vals, int64_t n, int32_t D, int32_t d, double sign,
+                              int64_t k, int32_t bits, uint64_t *key_out, void *ws, void *stream) {
+  HOI_CHECK_ARG(vals && key_out && ws && d >= 0 && d < D && k >= 1 && n >= 0 && bits >= 1,
+                "hoi_topk_bound: bad args");
+  return topk_key(vals, n, D, d, sign, k, bits, key_out, ws, (cudaStream_t)stream);
+}
+
+static int topk_key(const double *vals, int64_t n, int32_t D, int32_t d, double sign, int64_t k,
+                    int bits_wanted, uint64_t *key_out, void *ws, cudaStream_t s) {
   unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
   std::vector<unsigned long long> h(kRadixBins);
   uint64_t prefix = 0, hi_mask = 0;
@@ -510,6 +527,10 @@ extern "C" int hoi_topk_threshold(const double *vals, int64_t n, int32_t D, int3
       prefix |= (uint64_t)b << sh;
       hi_mask |= (uint64_t)((1 << bits) - 1) << sh;
       if (sh == 0) break;
+      if (64 - sh >= bits_wanted) {               // bound: the end of the bucket
+        prefix |= (1ull << sh) - 1;
+        break;
+      }
     }
     key = prefix;
   }
