@@ -468,6 +468,29 @@ def test_lattice_dataset_stacks(oracle):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("n,d", [(12, 5), (23, 3)])
+def test_lattice_dataset_stacks_at_the_size_limits(oracle, n, d):
+    """Dataset stacks at the smallest lattice (N = 12: 4 blocks per dataset)
+    and the largest stacked size (N = 23, just below the two-pass split):
+    vs the oracle at N = 12, vs the per-n-plet engine at N = 23."""
+    sigs = np.stack([0.7 * workloads.randcorr(n, np.random.default_rng(60 + s)) + 0.3 * np.eye(n)
+                     for s in range(d)])
+    ts = [300 + 11 * s for s in range(d)]
+    covs = hoi.CovSet([hoi.CovarianceMatrix(s, n_samples_used=t) for s, t in zip(sigs, ts)])
+    lo = 2 if n == 12 else 18
+    a = hoi.scan_device(covs, lo, n, bias_correct=True, engine=2).out
+    if n == 12:
+        _, vals = oracle.scan(sigs, ts, lo, n, oracle.CollectR(), bias=True)
+        np.testing.assert_allclose(a.cpu().numpy(), vals, rtol=RTOL, atol=ATOL)
+    else:
+        b = hoi.scan_device(covs, lo, n, bias_correct=True, engine=1).out
+        err = (a - b).abs() - 1e-9 * b.abs()
+        assert float(err.max()) <= 1e-11
+        del b
+    del a
+    torch.cuda.empty_cache()
+
+
 def test_lattice_scans_are_deterministic():
     """Repeated multi-dataset lattice scans are bit-identical.  Regression:
     when consumers lagged (D >= 4, strided output stores) a ring slot could
