@@ -31,10 +31,20 @@ namespace {
 constexpr int kGWarps = 4;   // warps per CTA
 
 template <int G, int M>
-struct __align__(16) GrpSmem {         // one per unit (group); 16-byte vector accesses
-  double vec[2][G * M + 2];            // broadcast vector, double-buffered by step parity
-  double red[G][G * M + 1];            // column partials of the inverse diagonal
-  int idx[G * M];                      // variable ids of the unit's n-plet
+struct GrpCore {                       // one per unit (group); 16-byte vector accesses
+  double vec[2][G * M + 2];            // broadcast vector, double-buffered by step (pair) parity
+  double red[G][G * M];                // column partials of the inverse diagonal; during the
+                                       // blocked LDL its first two rows hold column j+1 (even
+                                       // row length: 16-byte aligned rows)
+  int idx[G * M + ((G * M) & 3 ? 4 - ((G * M) & 3) : 0)];   // variable ids (16-byte multiple)
+};
+// Unit stride an odd multiple of 16 bytes: the 32/G groups of a warp read
+// their broadcast vectors at the same offset, and a stride that is a
+// multiple of 128 B put them all on the same banks (an 8-way conflict that
+// cost (4,6) a third of its speed).
+template <int G, int M>
+struct __align__(16) GrpSmem : GrpCore<G, M> {
+  char pad[sizeof(GrpCore<G, M>) % 32 == 16 ? 32 : 16];
 };
 
 template <int G>
@@ -47,6 +57,11 @@ __device__ __forceinline__ double group_sum(double v, unsigned gmask) {
 template <int G, int M, int MINB, bool COMPAT, bool SMEM>
 __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs A, int K) {
   constexpr int KT = G * M, U = 32 / G, S = G * M * (M + 1) / 2;
+  // LDL^T two columns per broadcast where the extra live values fit in
+  // registers; measured on B200 (cfg4 order segments): (2,9) K 17-18
+  // 3.2-3.7 -> 4.4-5.2 TF/s, (4,5) K 19-20 +4%; (4,6) and (4,7) run 2-5%
+  // slower blocked (more spills), so they keep one column per broadcast.
+  constexpr bool kBlocked2 = G == 2 || (G == 4 && M == 5);
   extern __shared__ __align__(16) double dynR[];
   __shared__ __align__(16) GrpSmem<G, M> usm[kGWarps * U];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -153,39 +168,116 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
       double dinv[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) dinv[m] = 1.0;
+      if constexpr (kBlocked2) {
+        // two columns per broadcast: columns j and j+1 are published as they
+        // stand before step j; every thread derives the step-j update of
+        // column j+1 (a'[c][j+1] = a[c][j+1] - a[c][j] l_(j+1)j) and applies
+        // both rank-1 updates to its rows -- one group sync per two columns.
 #pragma unroll
-      for (int j = 0; j < KT; ++j) {
-        if (j < K) {
-          double *vec = sm.vec[j & 1];
+        for (int j = 0; j < KT; j += 2) {
+          if (j < K) {
+            const bool two = j + 1 < K;
+            double *v0 = sm.vec[(j >> 1) & 1];
+            double *v1 = sm.red[(j >> 1) & 1];
 #pragma unroll
-          for (int m = 0; m < M; ++m)
-            if (G * (m + 1) > j) vec[t + G * m] = a[G * m * (m + 1) / 2 + j];
-          __syncwarp(gmask);
-          const double dj = vec[j];
-          if (!(dj > 0.0)) {
-            good = false;
-            break;
-          }
-          pd.mul(dj);
-          if ((j & 7) == 7) pd.renorm();
-          const double rp = __drcp_rn(dj);
-          if (t == j % G) dinv[j / G] = rp;
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            if (G * (m + 1) > j + 1) {         // the slot has rows below j
+            for (int m = 0; m < M; ++m) {
               const int o = G * m * (m + 1) / 2;
-              const double lij = a[o + j] * rp;
+              if (G * (m + 1) > j) v0[t + G * m] = a[o + j];
+              if (G * (m + 1) > j + 1) v1[t + G * m] = a[o + j + 1];
+            }
+            __syncwarp(gmask);
+            const double dj = v0[j];
+            if (!(dj > 0.0)) {
+              good = false;
+              break;
+            }
+            pd.mul(dj);
+            const double rp = __drcp_rn(dj);
+            if (t == j % G) dinv[j / G] = rp;
+            if (!two) {
 #pragma unroll
-              for (int c = (j + 1) & ~1; c < G * (m + 1); c += 2) {
-                const double2 v = *reinterpret_cast<const double2 *>(vec + c);
-                if (c > j) a[o + c] = fma(-lij, v.x, a[o + c]);
-                a[o + c + 1] = fma(-lij, v.y, a[o + c + 1]);
+              for (int m = 0; m < M; ++m) {
+                if (G * (m + 1) > j + 1) {
+                  const int o = G * m * (m + 1) / 2;
+                  const double lij = a[o + j] * rp;
+#pragma unroll
+                  for (int c = j + 2; c < G * (m + 1); c += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(v0 + c);
+                    a[o + c] = fma(-lij, v.x, a[o + c]);
+                    a[o + c + 1] = fma(-lij, v.y, a[o + c + 1]);
+                  }
+                  a[o + j + 1] = fma(-lij, v0[j + 1], a[o + j + 1]);
+                  a[o + j] = lij;
+                }
               }
-              a[o + j] = lij;
+              continue;
+            }
+            const double u = v0[j + 1];              // a[j+1][j]
+            const double l10 = u * rp;               // L[j+1][j]
+            const double dj1 = fma(-u, l10, v1[j + 1]);
+            if (!(dj1 > 0.0)) {
+              good = false;
+              break;
+            }
+            pd.mul(dj1);
+            if ((j & 7) == 6) pd.renorm();
+            const double rp1 = __drcp_rn(dj1);
+            if (t == (j + 1) % G) dinv[(j + 1) / G] = rp1;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (G * (m + 1) > j + 1) {             // the slot has rows below j
+                const int o = G * m * (m + 1) / 2;
+                const double lij = a[o + j] * rp;
+                const double li1 = fma(-lij, u, a[o + j + 1]) * rp1;
+#pragma unroll
+                for (int c = j + 2; c < G * (m + 1); c += 2) {
+                  const double2 w0 = *reinterpret_cast<const double2 *>(v0 + c);
+                  const double2 w1 = *reinterpret_cast<const double2 *>(v1 + c);
+                  const double n0 = fma(-w0.x, l10, w1.x), n1 = fma(-w0.y, l10, w1.y);
+                  a[o + c] = fma(-li1, n0, fma(-lij, w0.x, a[o + c]));
+                  a[o + c + 1] = fma(-li1, n1, fma(-lij, w0.y, a[o + c + 1]));
+                }
+                a[o + j] = lij;
+                a[o + j + 1] = li1;
+              }
             }
           }
         }
-      }
+      } else {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          if (j < K) {
+            double *vec = sm.vec[j & 1];
+  #pragma unroll
+            for (int m = 0; m < M; ++m)
+              if (G * (m + 1) > j) vec[t + G * m] = a[G * m * (m + 1) / 2 + j];
+            __syncwarp(gmask);
+            const double dj = vec[j];
+            if (!(dj > 0.0)) {
+              good = false;
+              break;
+            }
+            pd.mul(dj);
+            if ((j & 7) == 7) pd.renorm();
+            const double rp = __drcp_rn(dj);
+            if (t == j % G) dinv[j / G] = rp;
+  #pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (G * (m + 1) > j + 1) {         // the slot has rows below j
+                const int o = G * m * (m + 1) / 2;
+                const double lij = a[o + j] * rp;
+  #pragma unroll
+                for (int c = (j + 1) & ~1; c < G * (m + 1); c += 2) {
+                  const double2 v = *reinterpret_cast<const double2 *>(vec + c);
+                  if (c > j) a[o + c] = fma(-lij, v.x, a[o + c]);
+                  a[o + c + 1] = fma(-lij, v.y, a[o + c + 1]);
+                }
+                a[o + j] = lij;
+              }
+            }
+          }
+        }
+        }
       if (!good) {
         __syncwarp(gmask);
         continue;
