@@ -718,10 +718,11 @@ def _topk_host_slices(ctx, reducer, out, g0, d, step=1 << 20):
 def _topk_lattice(ctx, reducer, m_idx, shard=0, shard_bits=0, shard_mask=None):
     """TopK over an exhaustive scan without writing the full output (lattice
     engine): per dataset, (1) build the log-det table; (2) run the filtered
-    stencil over every 256th table block with no threshold and take the
-    exact k-th smallest key of that sample -- any subset's k-th smallest
-    key bounds the global k-th smallest from above, so every true top-k
-    n-plet passes it; (3) one filtered stencil pass over all blocks keeps
+    stencil over a hash-sampled 1/256 of the table blocks with no threshold
+    and take an upper bound of the k-th smallest key of that sample (its
+    top 36 bits resolved) -- any subset's k-th smallest key bounds the
+    global k-th smallest from above, so every true top-k n-plet passes it;
+    (3) one filtered stencil pass over all blocks keeps
     only the n-plets at or under that key; (4) an exact radix select over
     those candidates hands the k best (plus every tie at the k-th key) to
     the reference's host merge (sign*value, index tuple).  Returns False
