@@ -61,7 +61,7 @@ constexpr int kMinNearBits = 12;
 //                           chunked two-stream table/stencil pipeline
 struct LatticeTuning {
   int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
-  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1, lowsum_ring6 = 1;
+  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1, lowsum_ring6 = 1, extra_first = 1;
   LatticeTuning() {
     auto get = [](const char *name, int &v) {
       if (const char *e = getenv(name)) v = atoi(e);
@@ -78,6 +78,7 @@ struct LatticeTuning {
     get("HOI_STENCIL_PER_SM", stencil_per_sm);
     get("HOI_FILTER_RING6", filter_ring6);
     get("HOI_LOWSUM_RING6", lowsum_ring6);
+    get("HOI_EXTRA_FIRST", extra_first);
   }
 };
 
@@ -570,6 +571,7 @@ struct StencilPass {
   const unsigned *nlist;
   int prefetch;       // claim-ahead L2 prefetch of the own / pass-1-sum blocks
   unsigned nstack;    // > 0: a stack of that many datasets' tables (see claim())
+  int extra_first;    // issue the partial-sum job before the neighbours
 };
 
 // Compact the flagged blocks into a list in claim order (natural, or
@@ -685,6 +687,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   const unsigned nbmask = ps.nbmask;
   const int nP = N - CB;
   const bool pf_own = ps.prefetch != 0;
+  const bool tuning_extra_first = ps.extra_first != 0;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------ producer ----
@@ -738,8 +741,10 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       look[kLook - 1] = P == kEndBlock ? kEndBlock : claim();
       prefetch(look[kLook - 1]);
       unsigned prem = P == kEndBlock ? 0u : (P & nbmask);
-      // jobs of P: neighbours (far bits first), the partial-sum block, the own block
-      int stage = prem ? 0 : (ps.extra ? 1 : (OWN ? 2 : 3));
+      // jobs of P: [the partial-sum block,] neighbours (far bits first), the
+      // own block.  The DRAM-sourced partial sums go first so their load can
+      // start in a slot freed during the previous block's epilogue.
+      int stage = (ps.extra && tuning_extra_first) ? 1 : (prem ? 0 : (ps.extra ? 1 : (OWN ? 2 : 3)));
       for (bool first = true;; first = false) {
         const int slot = pJ % kRing;
         if (pJ >= kRing) mbar_wait(&sm.empty[slot], ((pJ / kRing) - 1) & 1u);
@@ -755,10 +760,10 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
           prem &= ~(1u << j);
           srcp = table + (int64_t)(P ^ (1u << j)) * BLK;
           pol = j >= near_bits ? pol_far : pol_near;
-          if (!prem) stage = ps.extra ? 1 : (OWN ? 2 : 4);
+          if (!prem) stage = (ps.extra && !tuning_extra_first) ? 1 : (OWN ? 2 : 4);
         } else if (stage == 1) {
           srcp = ps.extra + (int64_t)P * BLK;
-          stage = OWN ? 2 : 4;
+          stage = tuning_extra_first ? (prem ? 0 : (OWN ? 2 : 4)) : (OWN ? 2 : 4);
         } else if (stage == 2) {
           srcp = table + (int64_t)P * BLK;
           pol = pol_own;
@@ -1547,7 +1552,7 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
                                                   near_bits, own_last, per_sm_cap, none, p1, s);
     if (st) return st;
     ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
-                     listed ? cnts + 1 : nullptr, pf};
+                     listed ? cnts + 1 : nullptr, pf, 0u, tuning().extra_first};
   }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
   // Filter mode finishes entries from registers (no neighbour-sum buffer),
