@@ -1,6 +1,6 @@
 # Round evidence: GPU tests, full bench, launch list, ncu captures of the top kernels (one GPU)
 mkdir -p gpurun_out
-P=${PROF_TAG:-r01k}
+P=${PROF_TAG:-r01l}
 timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/${P}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_pytest.log
 timeout 300 python __graft_entry__.py > gpurun_out/${P}_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_smoke.log
 timeout 900 python bench.py > gpurun_out/${P}_bench.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_bench.log
