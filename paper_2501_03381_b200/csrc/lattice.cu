@@ -59,9 +59,13 @@ constexpr int kMinNearBits = 12;
 //   HOI_PREFETCH 0|1        claim-ahead L2 prefetch of DRAM-sourced blocks
 //   HOI_PIPE 0|1 (+ HOI_PIPE_WB, HOI_TABLE_NW, HOI_STENCIL_PER_SM)
 //                           chunked two-stream table/stencil pipeline
+//   HOI_FILTER_RING6 0|1    TopK filter on the 6-slot buffer-free ring
+//   HOI_LOWSUM_RING6 0|1    low-sum pass (pass 1) on the 6-slot buffer-free ring
+//   HOI_EXTRA_FIRST 0|1     pass 2 issues the pass-1-sum job before the neighbours
 struct LatticeTuning {
   int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
-  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3, filter_ring6 = 1, lowsum_ring6 = 1, extra_first = 1;
+  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3;
+  int filter_ring6 = 1, lowsum_ring6 = 1, extra_first = 1;
   LatticeTuning() {
     auto get = [](const char *name, int &v) {
       if (const char *e = getenv(name)) v = atoi(e);
