@@ -638,6 +638,29 @@ def test_block_shard_sets_reassemble_the_scan(world):
     torch.cuda.empty_cache()
 
 
+def test_topk_bound_brackets_the_exact_key():
+    """hoi_topk_bound: never below the exact k-th key (hoi_topk_threshold),
+    tighter with more bits, equal to it at 64 bits."""
+    import ctypes
+    rng = np.random.default_rng(3)
+    vals = torch.as_tensor(rng.standard_normal((50000, 5)), device="cuda")
+    lib, s = _native.lib(), _native.stream_handle(torch)
+    ws = torch.empty(4096 + 64, dtype=torch.int64, device="cuda")
+    key = torch.empty(1, dtype=torch.int64, device="cuda")
+    for sign, k in ((1.0, 1000), (-1.0, 7)):
+        _native.check(lib.hoi_topk_threshold(vals.data_ptr(), 50000, 5, 2, sign, k,
+                                             key.data_ptr(), ws.data_ptr(), s), "threshold")
+        exact = int(key.item()) & (2 ** 64 - 1)
+        prev = None
+        for bits in (12, 24, 36, 64):
+            _native.check(lib.hoi_topk_bound(vals.data_ptr(), 50000, 5, 2, sign, k, bits,
+                                             key.data_ptr(), ws.data_ptr(), s), "bound")
+            b = int(key.item()) & (2 ** 64 - 1)
+            assert b >= exact and (prev is None or b <= prev)
+            prev = b
+        assert prev == exact
+
+
 def test_topk_batch_matches_host_reducer():
     """Device batched TopK == the reference's TopK.update on the same
     HoiBatch (cfg5-style: 16 datasets, N = 400, order-10 random n-plets)."""
