@@ -60,6 +60,10 @@ __global__ void k_unrank_list(int N, int kmin, int kmax, const int64_t *__restri
 }
 
 // -------------------------------------------------------- mask compaction --
+// Rows are bucketed by order (popcount over W words); the per-order
+// kernels take orders <= 64, so orders above land in the last bucket and
+// are refused.
+constexpr int kMaskOrders = 72;
 __global__ void k_mask_orders(const uint64_t *__restrict__ masks, int W, int64_t B,
                               int32_t *__restrict__ order, int32_t *__restrict__ hist) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -67,7 +71,7 @@ __global__ void k_mask_orders(const uint64_t *__restrict__ masks, int W, int64_t
   int k = 0;
   for (int w = 0; w < W; ++w) k += __popcll(masks[b * W + w]);
   order[b] = k;
-  atomicAdd(&hist[k], 1);
+  atomicAdd(&hist[k < kMaskOrders - 1 ? k : kMaskOrders - 1], 1);   // last slot: order > 64
 }
 
 __global__ void k_mask_scatter(const uint64_t *__restrict__ masks, int W, int N, int64_t B,
@@ -149,7 +153,6 @@ extern "C" int hoi_eval_masks(const double *corr, const double *sdiag, const dou
                               int32_t err_cap, void *stream) {
   HOI_CHECK_ARG(corr && masks && err_count && N >= 1 && N <= 64 * W && D >= 1,
                 "hoi_eval_masks: bad args");
-  HOI_CHECK_ARG(N <= 64, "hoi_eval_masks: N > 64 is not supported");
   if (B == 0) return HOI_OK;
   cudaStream_t s = (cudaStream_t)stream;
   // compaction workspace (stream-ordered allocation; mask batches are not
@@ -177,13 +180,18 @@ extern "C" int hoi_eval_masks(const double *corr, const double *sdiag, const dou
       st = fail(HOI_INVALID_ARG, "hoi_eval_masks: empty mask row");
       goto done;
     }
+    for (int k = 65; k < kMaskOrders; ++k)
+      if (h[k] != 0) {
+        st = fail(HOI_INVALID_ARG, "hoi_eval_masks: mask rows of order > 64 are not supported");
+        goto done;
+      }
     int32_t off[72];
     int acc = 0;
     for (int k = 0; k < 72; ++k) { off[k] = acc; acc += h[k]; }
     cudaMemcpyAsync(cursor, off, sizeof(off), cudaMemcpyHostToDevice, s);
     k_mask_scatter<<<grid_for(B, 256), 256, 0, s>>>(masks, W, N, B, order, cursor, idx_sorted, row_map);
     if ((st = check_launch("k_mask_scatter"))) goto done;
-    for (int k = 1; k <= N && !st; ++k) {
+    for (int k = 1; k <= N && k <= 64 && !st; ++k) {
       if (h[k] == 0) continue;
       HOI_CHECK_ARG(!eta || kstride > k, "hoi_eval_masks: bias table too short");
       EvalArgs A{};

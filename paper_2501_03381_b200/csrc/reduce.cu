@@ -64,16 +64,20 @@ __global__ void k_topk_filter(const double *__restrict__ vals, int64_t n, int D,
   }
 }
 
-// Radix-select histogram: 12-bit digit at `shift` of the orderable key of
-// sign*vals[p*D+d] over the elements whose key bits above shift+12 equal
-// `prefix` (masked by `hi_mask`).
+// Radix-select histogram: the `bits`-wide digit (<= 12) at `shift` of the
+// orderable key of sign*vals[p*D+d] over the elements whose already
+// resolved key bits equal `prefix` (masked by `hi_mask`).  The digit is
+// masked to `bits`: the last round of a 64-bit select is 4 bits wide at
+// shift 0, and bits 4..11 there are part of the resolved prefix.
 constexpr int kRadixBits = 12;
 constexpr int kRadixBins = 1 << kRadixBits;
 
 __global__ void __launch_bounds__(512)
 k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double sign,
-             uint64_t prefix, uint64_t hi_mask, int shift, unsigned long long *__restrict__ counts) {
+             uint64_t prefix, uint64_t hi_mask, int shift, int bits,
+             unsigned long long *__restrict__ counts) {
   __shared__ unsigned int h[kRadixBins];
+  const uint64_t digit_mask = (1ull << bits) - 1;
   for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
   int cur = -1;
@@ -82,7 +86,7 @@ k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double si
        p += (int64_t)gridDim.x * blockDim.x) {
     uint64_t key = orderable_key(sign * vals[p * D + d]);
     if ((key & hi_mask) != prefix) continue;
-    const int b = (int)((key >> shift) & (kRadixBins - 1));
+    const int b = (int)((key >> shift) & digit_mask);
     if (b == cur) {
       ++run;
     } else {
@@ -371,7 +375,7 @@ extern "C" int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t
       int sh = shift < 0 ? 0 : shift;
       int bits = shift < 0 ? kRadixBits + shift : kRadixBits;
       cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kRadixBins, s);
-      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, counts);
+      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, bits, counts);
       int st = check_launch("k_radix_hist");
       if (st) return st;
       cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * kRadixBins,
@@ -511,7 +515,7 @@ static int topk_key(const double *vals, int64_t n, int32_t D, int32_t d, double 
       const int sh = shift < 0 ? 0 : shift;
       const int bits = shift < 0 ? kRadixBits + shift : kRadixBits;
       cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kRadixBins, s);
-      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, counts);
+      k_radix_hist<<<blocks, 512, 0, s>>>(vals, n, D, d, sign, prefix, hi_mask, sh, bits, counts);
       int st = check_launch("k_radix_hist");
       if (st) return st;
       cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * kRadixBins,

@@ -10,6 +10,7 @@ single jitter retry.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import math
 from dataclasses import dataclass
 
@@ -114,7 +115,15 @@ def enumerate_order(n: int, k: int, batch_size: int = 10000):
         raise InvalidData(f"batch_size must be >= 1, got {batch_size}")
     total = math.comb(n, k)
     if n > 64:
-        raise InvalidOrderRange("enumeration supports N <= 64")
+        # beyond the device unranking table (64-bit binomials, N <= 64): the
+        # reference's own itertools walk, same batches
+        it = itertools.combinations(range(n), k)
+        while True:
+            flat = np.fromiter(itertools.chain.from_iterable(itertools.islice(it, batch_size)),
+                               dtype=np.int64)
+            if flat.size == 0:
+                return
+            yield NpletBatch(n, indices=flat.reshape(-1, k), check_unique=False)
     chunk = max(batch_size, min(1 << 22, (total // batch_size + 1) * batch_size))
     chunk = (chunk // batch_size) * batch_size
     g = 0

@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes
 import functools
 import gc
+import itertools
 import math
 import time
 from dataclasses import dataclass
@@ -505,13 +506,53 @@ def scan_device(covs: CovSet, min_order: int, max_order: int, *, bias_correct: b
     ``scan(..., Callback(...))`` without leaving HBM)."""
     n = covs.n_variables
     total = count_nplets(n, min_order, max_order)
-    if n > 64:
-        raise InvalidOrderRange("scan_device supports N <= 64")
     g_end = total if g_end is None else g_end
+    if not 0 <= g_begin <= g_end <= total:
+        raise InvalidData(f"rank range [{g_begin}, {g_end}) outside [0, {total})")
+    if n > 64:
+        # beyond the device unranking table: host-enumerated index batches
+        # (the reference's itertools order), measures computed on the device
+        # straight into the resident output
+        from .nplet_engine import eval_device
+        torch = nat.torch_cuda()
+        d = covs.n_datasets
+        o = out if out is not None else torch.empty((4, g_end - g_begin, d),
+                                                    dtype=torch.float64, device="cuda")
+        for r0, k, idx in _host_batches(n, min_order, max_order, 1 << 18, g_begin, g_end):
+            h, _, _ = eval_device(covs, NpletBatch(n, indices=idx, check_unique=False),
+                                  bias_correct, measures=True)
+            o[:, r0 - g_begin:r0 - g_begin + idx.shape[0]] = h
+        return DeviceScan(o, n, min_order, max_order, g_begin, g_end)
     ctx = _ScanCtx(covs, min_order, max_order, bias_correct, engine)
     o, cnt, coords = ctx.full(g_begin, g_end, out)
     _raise_not_pd(cnt, coords)
     return DeviceScan(o, n, min_order, max_order, g_begin, g_end)
+
+
+def _host_batches(n, lo, hi, batch_size, g_begin=0, g_end=None):
+    """(global rank of the first row, order, (m, k) int64 indices) for the
+    rows [g_begin, g_end) of the order-major lexicographic scan, batches of
+    at most batch_size rows never crossing an order, from itertools (the
+    reference's enumeration, ref:nplet_engine.py:128-136; used for N > 64)."""
+    off = 0
+    for k in range(lo, hi + 1):
+        c = math.comb(n, k)
+        a = max(g_begin - off, 0)
+        b = c if g_end is None else min(c, g_end - off)
+        if a < b:
+            it = itertools.islice(itertools.combinations(range(n), k), a, b)
+            g = off + a
+            while True:
+                flat = np.fromiter(itertools.chain.from_iterable(itertools.islice(it, batch_size)),
+                                   dtype=np.int64)
+                if flat.size == 0:
+                    break
+                idx = flat.reshape(-1, k)
+                yield g, k, idx
+                g += idx.shape[0]
+        off += c
+        if g_end is not None and off >= g_end:
+            return
 
 
 def _batch_bounds(n, lo, hi, batch_size):
@@ -951,24 +992,16 @@ def scan(covs: CovSet, min_order: int, max_order: int, reducer: Reducer, *,
     t0 = time.perf_counter()
     if n > 64:
         # beyond the unranking table: host-enumerated batches, device math
-        from .nplet_engine import enumerate_order  # noqa: F401  (N <= 64 only)
-        import itertools
         seen = 0
         nb = 0
-        for k in range(min_order, max_order + 1):
-            it = itertools.combinations(range(n), k)
-            while True:
-                flat = np.fromiter(itertools.chain.from_iterable(itertools.islice(it, batch_size)),
-                                   dtype=np.int64)
-                if flat.size == 0:
-                    break
-                batch = NpletBatch(n, indices=flat.reshape(-1, k), check_unique=False)
-                reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct=bias_correct))
-                nb += 1
-                seen += batch.batch_size
-                if progress is not None:
-                    progress({"batches": nb, "nplets": seen, "total": total, "order": k,
-                              "elapsed": time.perf_counter() - t0})
+        for _, k, idx in _host_batches(n, min_order, max_order, batch_size):
+            batch = NpletBatch(n, indices=idx, check_unique=False)
+            reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct=bias_correct))
+            nb += 1
+            seen += batch.batch_size
+            if progress is not None:
+                progress({"batches": nb, "nplets": seen, "total": total, "order": k,
+                          "elapsed": time.perf_counter() - t0})
         return reducer.finalize()
     ctx = _ScanCtx(covs, min_order, max_order, bias_correct)
     if type(reducer) in (TopK, Histogram):

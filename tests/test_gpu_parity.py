@@ -17,6 +17,8 @@ import paper_2501_03381_b200 as hoi
 from paper_2501_03381_b200 import _build, _native, workloads
 from paper_2501_03381_b200.nplet_engine import _batched_logdet_invdiag, unrank_device
 
+import hoi_oracle as ora  # checker only (analytic R/S fixtures)
+
 pytestmark = pytest.mark.gpu
 RTOL, ATOL = 1e-9, 1e-11
 
@@ -169,8 +171,8 @@ def test_identity_exact_zeros_and_closed_forms(golden):
         for m in (h.tc, h.dtc, h.o, h.s):
             assert (m == 0.0).all()
     for m in (2, 3, 4):
-        for kind, fn in (("r", hoi.r_system_cov), ("s", hoi.s_system_cov)):
-            cov = fn(m, 1.0)
+        for kind, fn in (("r", ora.r_system), ("s", ora.s_system)):
+            cov = hoi.CovarianceMatrix(fn(m, 1.0))
             h = hoi.compute_hoi_batch(hoi.CovSet([cov]),
                                       hoi.NpletBatch(m + 1, indices=np.arange(m + 1)[None]))
             np.testing.assert_allclose([h.tc[0, 0], h.dtc[0, 0], h.o[0, 0], h.s[0, 0]],
@@ -296,7 +298,7 @@ def test_features_and_callback_order(golden):
     for f, w in zip(feats, red["features_t7"]):
         for name, v in w.items():
             assert getattr(f, name) == pytest.approx(v, abs=1e-12), name
-    for f, w in zip(hoi.extract_features(hoi.CovSet([hoi.r_system_cov(3, 1.0)])), red["features_r3"]):
+    for f, w in zip(hoi.extract_features(hoi.CovSet([hoi.CovarianceMatrix(ora.r_system(3, 1.0))])), red["features_r3"]):
         for name, v in w.items():
             assert getattr(f, name) == pytest.approx(v, abs=1e-12), name
     ident = hoi.extract_features(hoi.CovSet([hoi.CovarianceMatrix(np.eye(5))]))[0]

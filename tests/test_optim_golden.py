@@ -1,5 +1,5 @@
-"""Optimiser drop-in (ref:optimizers.py) and PgmSpec
-(ref:synthetic.py) against results of the real reference
+"""Optimiser drop-in (ref:optimizers.py) against
+results of the real reference
 (tests/golden/make_golden_optim.py).  Host-only checks run on CPU; the
 greedy / anneal runs evaluate every energy on the device (-m gpu)."""
 
@@ -27,17 +27,6 @@ SPECS = {
     "mean_s_min": hoi.ObjectiveSpec("s", "min"),
     "effect_tc_max": hoi.ObjectiveSpec("tc", "max", "effect", (0, 1), (2, 3)),
 }
-
-
-def test_pgm_spec_round_trip():
-    spec = hoi.PgmSpec.from_json(GOLD["pgm_json"])
-    assert spec.to_json() == GOLD["pgm_json"]
-    assert spec.variable_names() == GOLD["pgm_names"]
-    assert spec.n_variables == GOLD["pgm_n"] == spec.build().n_variables
-    for bad in ('{"blocks": []}', '{"blocks": [{"kind": "q", "n_sources": 2}]}', "[1]",
-                '{"blocks": [{"kind": "r", "n_sources": 2, "x": 1}]}', "{nope"):
-        with pytest.raises(hoi.InvalidData):
-            hoi.PgmSpec.from_json(bad)
 
 
 def test_objective_spec_validation():
