@@ -116,6 +116,16 @@ int hoi_eval_indices(const double *corr, const double *sdiag, const double *eta,
                      double *invdiag, int32_t *err_count, int64_t *err_coords,
                      int32_t err_cap, void *stream);
 
+/* hoi_eval_indices (measures only) into rows [0, B) of a larger output
+ * whose planes are out_plane elements apart: one chunk of a (4, rows, D)
+ * result (pass out + r0 * D).  Lets a large host index batch stream to the
+ * device chunk by chunk, each chunk's kernel overlapping the next chunk's
+ * upload.  Error rows are chunk-relative. */
+int hoi_eval_indices_into(const double *corr, const double *sdiag, const double *eta,
+                          int32_t kstride, int32_t N, int32_t D, const int32_t *idx, int64_t B,
+                          int32_t K, double *out, int64_t out_plane, int32_t *err_count,
+                          int64_t *err_coords, int32_t err_cap, void *stream);
+
 /* Mixed-order (mask) batches: masks (B, W) uint64 words (bit j of word j/64
  * = variable j).  Equivalent to identity padding (ref:nplet_engine.py:204-224,
  * 332-351): each row is compacted to its members and evaluated at its own
@@ -243,13 +253,29 @@ int hoi_lattice_shard_set_filter(const double *corr, int32_t N, int32_t D, int32
                                  double *cand, int64_t cand_cap, uint64_t *count,
                                  int32_t build_table, void *ws, size_t ws_bytes, void *stream);
 
-/* Engine 3: both phases in ONE persistent pass (dataset d).  Warps claim
- * table blocks in increasing order, build and publish their block, then
- * acquire their (lower-index, already claimed) neighbour blocks and write
- * the measures.  Synchronous (returns HOI_FALLBACK if not PD). */
-int hoi_lattice_fused(const double *corr, int32_t N, int32_t D, int32_t d, const double *eta,
-                      int32_t kstride, int32_t kmin, int32_t kmax, int64_t g_begin,
-                      int64_t g_end, double *out, void *ws, size_t ws_bytes, void *stream);
+/* Multi-GPU FULL output with compact shards (ref:scanner.py:290-305's
+ * ordered merge, done by the caller): hoi_lattice_shard_set's n-plets
+ * written block-major to a LOCAL output -- local block c holds the 1024
+ * n-plets P u Q of table block P = blocks[c] in run order at rows
+ * c*1024 .. c*1024+1023 (rows of orders outside [kmin, kmax] are holes) --
+ * instead of at their global rows.  local_rows >= popcount(shard_mask) *
+ * 2^(N - shard_bits); out is 4 planes of (local_rows, D).  blocks (device,
+ * 2^(N-10) u32) and *nblocks (device int64) receive the block list.
+ * Asynchronous after the table's not-PD check. */
+int hoi_lattice_shard_local(const double *corr, int32_t N, int32_t D, int32_t d,
+                            const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
+                            uint64_t shard_mask, int32_t shard_bits, double *out,
+                            int64_t local_rows, uint32_t *blocks, int64_t *nblocks, void *ws,
+                            size_t ws_bytes, void *stream);
+/* Local rows -> global rows: every row of a hoi_lattice_shard_local output
+ * whose global rank lies in [g_begin, g_end) is copied to
+ * out[rank - g_begin] (4 planes of (g_end - g_begin, D)).  The receive side
+ * of the rank-ordered gather: the shards of all ranks, scattered into one
+ * output, equal the single-GPU scan bit for bit. */
+int hoi_lattice_local_scatter(const double *local, int64_t local_rows, const uint32_t *blocks,
+                              const int64_t *nblocks, int32_t N, int32_t D, int32_t kmin,
+                              int32_t kmax, int64_t g_begin, int64_t g_end, double *out,
+                              void *stream);
 
 /* ---------------------------------------------------------------------------
  * (5) Device reducers over a full-output plane (ref:scanner.py:50-137).
@@ -275,6 +301,17 @@ int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double 
 int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign, int64_t k,
                           int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
                           int64_t *h_counts, void *ws, void *stream);
+
+/* Exact TopK order of the candidates (ref:scanner.py:75-100, key
+ * (sign*value, index tuple) ascending) for every dataset of a fixed-order
+ * batch: CTA d sorts cand[d*cand_cap ...] (counts[d] of them, DEVICE int64
+ * array of D; cand_cap <= 8192) by the orderable key of sign*vals[p*D+d],
+ * equal keys by the lexicographic tuple idx[p*K .. p*K+K) (int32), equal
+ * tuples by p, and writes the first k positions to top_pos[d*k ...] (-1
+ * past counts[d]).  Asynchronous. */
+int hoi_topk_order(const double *vals, int32_t D, double sign, const int64_t *cand,
+                   int64_t cand_cap, const int64_t *counts, const int32_t *idx, int32_t K,
+                   int64_t k, int64_t *top_pos, void *stream);
 
 /* Exact k-th smallest key (the threshold step of TopK, ref:scanner.py:75-100):
  * the order-preserving 64-bit key of the k-th

@@ -37,6 +37,8 @@ _SIGS = {
     "hoi_correlation": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "hoi_eval_indices": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                           _vp, _i32, _vp], C.c_int),
+    "hoi_eval_indices_into": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _vp,
+                               _vp, _i32, _vp], C.c_int),
     "hoi_eval_indices_fp32": ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp,
                                _vp, _i32, _vp], C.c_int),
     "hoi_eval_masks": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _i64, _vp, _vp, _vp, _vp,
@@ -61,14 +63,17 @@ _SIGS = {
                             _vp, _i64, _vp, _vp], C.c_int),
     "hoi_lattice_measures": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp,
                               _vp], C.c_int),
-    "hoi_lattice_fused": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i64, _vp, _vp,
-                           _sz, _vp], C.c_int),
+    "hoi_lattice_shard_local": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _i32, C.c_uint64, _i32,
+                                 _vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
+    "hoi_lattice_local_scatter": ([_vp, _i64, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _vp,
+                                   _vp], C.c_int),
     "hoi_topk_select": ([_vp, _i64, _i32, _i32, _dbl, _i64, _i64, _vp, _i64, C.POINTER(_i64),
                          _vp, _vp], C.c_int),
     "hoi_topk_select_multi": ([_vp, _i64, _i32, _dbl, _i64, _i64, _vp, _i64, C.POINTER(_i64),
                                _vp, _vp], C.c_int),
     "hoi_features": ([_vp, _i64, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp], C.c_int),
     "hoi_objective": ([_vp, _i64, _i32, _i32, _vp, _vp, _i32, _dbl, _vp, _vp, _vp], C.c_int),
+    "hoi_topk_order": ([_vp, _i32, _dbl, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _vp], C.c_int),
     "hoi_topk_threshold": ([_vp, _i64, _i32, _i32, _dbl, _i64, _vp, _vp, _vp], C.c_int),
     "hoi_topk_bound": ([_vp, _i64, _i32, _i32, _dbl, _i64, _i32, _vp, _vp, _vp], C.c_int),
     "hoi_topk_filter": ([_vp, _i64, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _vp], C.c_int),

@@ -389,7 +389,7 @@ static int launch_one(const EvalArgs &A, int K, cudaStream_t s) {
 int launch_eval_k1_12(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_k13_16(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_generic(const EvalArgs &A, int K, cudaStream_t s);
-int launch_eval_warp(const EvalArgs &A, int K, cudaStream_t s);   // 17 <= K <= 32
 int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s);  // 17 <= K <= 32
+int launch_eval_pipe(const EvalArgs &A, int K, cudaStream_t s);   // 4 <= K <= 12, R in L2
 
 }  // namespace hoib

@@ -1,0 +1,225 @@
+// Engine 1, batched index mode with the correlation matrix in L2 (large N,
+// e.g. BASELINE config 5: N = 400, D = 16, order 10): a gather-pipelined
+// variant of k_eval for fixed orders 4..12.
+//
+// k_eval gathers the K(K-1)/2 off-diagonal entries of R_S straight into
+// registers and then factorises, so each warp sits idle for an L2 round
+// trip per unit and the register file holds the gathered values in flight
+// (168 registers, ~12 warps/SM, FP64 pipe ~49% busy at K = 10).  Here every
+// thread streams the NEXT unit's entries into its own shared-memory stage
+// with cp.async (8-byte LDGSTS, no registers held) while it factorises the
+// current one from the other stage: the L2 latency hides behind a unit of
+// FP64 work and the kernel runs FP64-bound at 8 warps/SM (two 128-thread
+// CTAs: 2 stages x K(K-1)/2 doubles x 128 threads of shared memory each).
+//
+// Stage layout [stage][entry][thread]: a warp's 32 threads touch 32
+// consecutive doubles per entry (conflict-free).  Threads keep a fixed
+// dataset d (grid x 128 is a multiple of D) and walk n-plets b, b + step/D,
+// ...; with the dataset index fastest in R (N, N, D), the 16 threads of a
+// config-5 n-plet read one 128-byte line per entry.
+//
+// Arithmetic per unit is k_eval's (ref:nplet_engine.py:267-281 restated as
+// LDL^T + unit-triangular inverse + inverse diagonal, ref:measures.py:41-81
+// epilogue) with two cheaper non-algorithmic pieces: the pivot reciprocal
+// is MUFU.RCP64H refined by one cubic Newton step (3 DFMA; |rel err| <
+// 2^-60, against __drcp_rn's correctly rounded multi-step sequence), and
+// the two log products go through k_eval's LogProd.  A non-positive pivot
+// reruns the unit through k_eval's jitter retry (ref:nplet_engine.py:237-264).
+#include "eval_kernels.cuh"
+
+namespace hoib {
+namespace {
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// 1/x for x > 0 normal: hardware approximation + one cubic Newton step
+// (e = 1 - x r; r' = r (1 + e + e^2)); the approximation's ~2^-22 error
+// cubes to below double precision.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+template <int K>
+__device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &pd) {
+  pd.init();
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double dj = a[TRI(j, j)];
+    if (!(dj > 0.0)) return false;
+    pd.mul(dj);
+    if ((j & 7) == 7) pd.renorm();
+    const double r = fast_rcp(dj);
+    a[TRI(j, j)] = r;
+#pragma unroll
+    for (int i = K - 1; i > j; --i) {
+      const double lij = a[TRI(i, j)] * r;
+#pragma unroll
+      for (int m = j + 1; m <= i; ++m) a[TRI(i, m)] = fma(-lij, a[TRI(m, j)], a[TRI(i, m)]);
+      a[TRI(i, j)] = lij;
+    }
+  }
+  pd.renorm();
+  return true;
+}
+
+// U = L^-1 in place, then lam = log prod_j (M^-1)_jj, (M^-1)_jj = sum_i U_ij^2 / d_i
+template <int K>
+__device__ __forceinline__ double inv_diag_logprod(double (&a)[K * (K + 1) / 2]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double acc = a[TRI(i, j)];
+#pragma unroll
+      for (int m = j + 1; m < i; ++m) acc = fma(a[TRI(i, m)], a[TRI(m, j)], acc);
+      a[TRI(i, j)] = -acc;
+    }
+  }
+  LogProd pl;
+  pl.init();
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double sacc = a[TRI(j, j)];
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      const double u = a[TRI(i, j)];
+      sacc = fma(u * u, a[TRI(i, i)], sacc);
+    }
+    pl.mul(sacc);
+    if ((j & 7) == 7) pl.renorm();
+  }
+  pl.renorm();
+  return pl.log_value();
+}
+
+constexpr int kPipeThreads = 128;
+
+template <int K>
+__global__ void __launch_bounds__(kPipeThreads, 3) k_eval_pipe(const EvalArgs A) {
+  constexpr int NE = K * (K - 1) / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *stage = reinterpret_cast<double *>(smem_raw) + threadIdx.x;
+  const int tid = threadIdx.x;
+  const int D = A.D, N = A.N;
+  const int64_t t0 = blockIdx.x * (int64_t)kPipeThreads + tid;
+  const int64_t step = (int64_t)gridDim.x * kPipeThreads;   // a multiple of D
+  const int d = (int)(t0 % D);
+  const int64_t db = step / D;
+  const double *Rd = A.src + d;
+  const int rowN = N * D;
+
+  // element offsets fit in 32 bits (N*N*D < 2^31, checked at launch): one
+  // integer add and one wide multiply-add per gathered element
+  auto issue = [&](int64_t b) {
+    if (b < A.B) {
+      const int32_t *ix = A.idx + b * A.idx_stride;
+      int col[K], row[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int v = __ldg(ix + i);
+        col[i] = v * D;
+        row[i] = v * rowN;
+      }
+#pragma unroll
+      for (int i = 1; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j)
+          cp_async8(stage + (TRI(i, j) - i) * kPipeThreads, Rd + (row[i] + col[j]));
+    }
+    cp_async_commit();
+  };
+
+  int64_t b = t0 / D;
+  issue(b);
+  const int s_dummy[K] = {};
+  const double cs_dummy[K] = {};
+  for (; b < A.B; b += db) {
+    cp_async_wait_all();
+    double a[K * (K + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+#pragma unroll
+      for (int j = 0; j < i; ++j) a[TRI(i, j)] = stage[(TRI(i, j) - i) * kPipeThreads];
+      a[TRI(i, i)] = 1.0;
+    }
+    LogProd pd;
+    const bool ok = ldl_fast<K>(a, pd);
+    // every staged value has been consumed by the factorisation (and the
+    // stage is only ever touched by this thread): the next unit's gather
+    // streams in behind the rest of this unit's work
+    issue(b + db);
+    if (!ok) {
+      eval_retry<K, true, false>(A, A.src, b, d, K);
+      continue;
+    }
+    const double lam = inv_diag_logprod<K>(a);
+    finish_unit<K, true, false>(A, b, d, K, s_dummy, true, pd.log_value(), lam, cs_dummy);
+  }
+}
+
+template <int K>
+int launch_pipe(const EvalArgs &A, cudaStream_t s) {
+  constexpr int NE = K * (K - 1) / 2;
+  const int smem = (int)(NE * kPipeThreads * sizeof(double));
+  static thread_local int cap_for = -1, cap = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cap_for != dev) {
+    cudaFuncSetAttribute(k_eval_pipe<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_pipe<K>, kPipeThreads, smem);
+    cap = sms * (per > 0 ? per : 1);
+    cap_for = dev;
+  }
+  // grid x 128 must be a multiple of D (each thread keeps its dataset)
+  int g = 1;
+  while ((g * kPipeThreads) % A.D) ++g;
+  const int64_t units = A.B * (int64_t)A.D;
+  int64_t want = (units + kPipeThreads - 1) / kPipeThreads;
+  int64_t grid = want < cap ? want : cap;
+  grid = ((grid + g - 1) / g) * g;
+  if (grid < 1) grid = g;
+  k_eval_pipe<K><<<(int)grid, kPipeThreads, smem, s>>>(A);
+  return check_launch("k_eval_pipe");
+}
+
+}  // namespace
+
+// -1 when the launch is not this kernel's (see nplet_eval.cu launch_eval):
+// fixed orders 4..12, FP64 measures only, index rows, R in global memory.
+int launch_eval_pipe(const EvalArgs &A, int K, cudaStream_t s) {
+  if (A.mats || !A.idx || A.fp32 || A.logdet || A.invdiag || A.row_map || !A.out) return -1;
+  if ((size_t)A.N * A.N * A.D * sizeof(double) <= (size_t)kEvalSmemMax) return -1;
+  if ((int64_t)A.N * A.N * A.D >= (1ll << 31)) return -1;
+  if (A.B * (int64_t)A.D < (int64_t)kPipeThreads * 148) return -1;   // small batches: k_eval
+  upload_binomials();
+  switch (K) {
+    case 4: return launch_pipe<4>(A, s);
+    case 5: return launch_pipe<5>(A, s);
+    case 6: return launch_pipe<6>(A, s);
+    case 7: return launch_pipe<7>(A, s);
+    case 8: return launch_pipe<8>(A, s);
+    case 9: return launch_pipe<9>(A, s);
+    case 10: return launch_pipe<10>(A, s);
+    case 11: return launch_pipe<11>(A, s);
+    case 12: return launch_pipe<12>(A, s);
+    default: return -1;
+  }
+}
+
+}  // namespace hoib

@@ -43,53 +43,20 @@ constexpr int MAXB = 6;           // prefix variables expanded inside one CTA
 // noise, so the engine declines and the per-n-plet engine (with the
 // reference's per-matrix jitter rule) takes the scan.
 constexpr double kMinPivot = 1e-12;
-// Block-index bits whose neighbour blocks lie beyond the L2 reuse window
-// (126 MB / 8 KB blocks ~ 2^14 blocks): streamed with evict-first loads.
-constexpr int kFarBits = 6;
-constexpr int kMinNearBits = 12;
-
-// Measurement knobs of the lattice engine, read once from the environment.
-// The defaults are the measured best on B200 (cfg4); the
-// alternatives stay selectable so those measurements can be repeated.
-//   HOI_RING 4|5|6          stencil ring slots per CTA (4: 4 CTAs x 4 slots)
-//   HOI_OWN_LAST 0|1        own block loaded with L2 evict_last
-//   HOI_NEAR_BITS b         neighbour bits >= b loaded evict-first (default: none)
-//   HOI_TWO_PASS 0|1        two-pass stencil for full output (N >= 24)
-//   HOI_TWO_PASS_FILTER 0|1 two-pass stencil for the TopK filter
-//   HOI_PREFETCH 0|1        claim-ahead L2 prefetch of DRAM-sourced blocks
-//   HOI_PIPE 0|1 (+ HOI_PIPE_WB, HOI_TABLE_NW, HOI_STENCIL_PER_SM)
-//                           chunked two-stream table/stencil pipeline
-//   HOI_FILTER_RING6 0|1    TopK filter on the 6-slot buffer-free ring
-//   HOI_LOWSUM_RING6 0|1    low-sum pass (pass 1) on the 6-slot buffer-free ring
-//   HOI_EXTRA_FIRST 0|1     pass 2 issues the pass-1-sum job before the neighbours
-struct LatticeTuning {
-  int ring = 4, own_last = 1, near_bits = -1, two_pass = 1, two_pass_filter = 0, prefetch = 0;
-  int pipe = 0, pipe_wb = 16, table_nw = 4, stencil_per_sm = 3;
-  int filter_ring6 = 1, lowsum_ring6 = 1, extra_first = 1;
-  LatticeTuning() {
-    auto get = [](const char *name, int &v) {
-      if (const char *e = getenv(name)) v = atoi(e);
-    };
-    get("HOI_RING", ring);
-    get("HOI_OWN_LAST", own_last);
-    get("HOI_NEAR_BITS", near_bits);
-    get("HOI_TWO_PASS", two_pass);
-    get("HOI_TWO_PASS_FILTER", two_pass_filter);
-    get("HOI_PREFETCH", prefetch);
-    get("HOI_PIPE", pipe);
-    get("HOI_PIPE_WB", pipe_wb);
-    get("HOI_TABLE_NW", table_nw);
-    get("HOI_STENCIL_PER_SM", stencil_per_sm);
-    get("HOI_FILTER_RING6", filter_ring6);
-    get("HOI_LOWSUM_RING6", lowsum_ring6);
-    get("HOI_EXTRA_FIRST", extra_first);
-  }
-};
-
-const LatticeTuning &tuning() {
-  static const LatticeTuning t;
-  return t;
-}
+// Stencil configuration: the measured best on B200 (cfg4).
+//   full output, pass 2 : 4-slot TMA ring, 4 CTAs/SM, double-buffered
+//                         neighbour sums (kRingFull / kCtasFull)
+//   low-sum pass 1 and the TopK filter: 6-slot ring, no neighbour-sum buffer
+//                         (entries finish from registers), 4 CTAs/SM
+//   own block loaded L2 evict_last; neighbour blocks evict_normal
+//   full output N >= 24: two passes split by prefix-bit groups; filter:
+//                         single pass (bound by per-job latency, not bytes)
+//   pass 2 issues the DRAM-sourced pass-1-sum job before the neighbours
+// Alternatives measured and dropped (round 1): 5/6-slot full rings, 3 or 2
+// CTAs/SM, evict-first far neighbours, claim-ahead L2 prefetch, a chunked
+// table/stencil two-stream pipeline and a single fused produce/consume
+// kernel -- all equal or slower.
+constexpr int kRingFull = 4, kCtasFull = 4, kRingLean = 6;
 
 __constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
@@ -401,9 +368,6 @@ __device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
                                             uint64_t *bar, uint64_t policy) {
   asm volatile(
@@ -573,9 +537,9 @@ struct StencilPass {
   int perm_lb;
   const unsigned *list;
   const unsigned *nlist;
-  int prefetch;       // claim-ahead L2 prefetch of the own / pass-1-sum blocks
   unsigned nstack;    // > 0: a stack of that many datasets' tables (see claim())
-  int extra_first;    // issue the partial-sum job before the neighbours
+  int local;          // MODE_FULL: write block-major local rows (claim index c:
+                      // rows c*1024 + run position) instead of global rows
 };
 
 // Compact the flagged blocks into a list in claim order (natural, or
@@ -656,6 +620,10 @@ k_write_blocks(const uint8_t *__restrict__ active, int nP, int perm_lb,
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count = base;
 }
 
+__global__ void k_count_to_i64(const unsigned *__restrict__ c, int64_t *__restrict__ out) {
+  *out = (int64_t)*c;
+}
+
 enum { MODE_FULL = 0, MODE_FILTER = 1, MODE_LOWSUM = 2 };
 
 template <int kRing, int kMinCtas, int MODE, int NB = 2>
@@ -664,13 +632,13 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
                    const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
                    int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
                    unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
-                   int near_bits, unsigned *__restrict__ counter, int own_last, StencilFilter flt,
-                   StencilPass ps) {
+                   unsigned *__restrict__ counter, StencilFilter flt, StencilPass ps) {
   constexpr bool FILTER = MODE == MODE_FILTER;
   constexpr bool OWN = MODE != MODE_LOWSUM;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StencilSmem<kRing, NB> &sm = *reinterpret_cast<StencilSmem<kRing, NB> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
+  __shared__ unsigned blkc[kBlkQ];                 // claim index of blkq's block (local rows)
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (OWN && NB == 2) {
@@ -690,22 +658,20 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   __syncthreads();
   const unsigned nbmask = ps.nbmask;
   const int nP = N - CB;
-  const bool pf_own = ps.prefetch != 0;
-  const bool tuning_extra_first = ps.extra_first != 0;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------ producer ----
     if (lane != 0) return;
-    const uint64_t pol_near = l2_policy(false), pol_far = l2_policy(true);
-    const uint64_t pol_own = own_last ? l2_policy_last() : pol_near;
+    const uint64_t pol_near = l2_policy(false), pol_own = l2_policy_last();
     const int hb = nP - ps.perm_lb;
+    unsigned c = 0;                                // claim index of the last claim
     auto claim = [&]() -> unsigned {
       if (ps.list) {
-        const unsigned c = atomicAdd(counter, 1u);
+        c = atomicAdd(counter, 1u);
         return c < *ps.nlist ? ps.list[c] : kEndBlock;
       }
       for (;;) {
-        const unsigned c = atomicAdd(counter, 1u);
+        c = atomicAdd(counter, 1u);
         if (c >= blk_end - blk_begin) return kEndBlock;
         if (ps.nstack > 0) {
           // stacked datasets, claimed 4 datasets per block: output rows are
@@ -721,38 +687,21 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
         if (!active || active[blk_begin + q]) return blk_begin + q;
       }
     };
-    // Claim-ahead queue: blocks are claimed kLook ahead of streaming and
-    // their DRAM-sourced 8 KB blocks (own T[P], and the pass-1 sums) are
-    // prefetched into L2 at claim time, so the in-order TMA ring only ever
-    // waits for L2 hits.
-    constexpr int kLook = 4;
-    unsigned look[kLook];
-    auto prefetch = [&](unsigned Q) {
-      if (Q == kEndBlock || !pf_own) return;
-      if (OWN) l2_prefetch(table + (int64_t)Q * BLK, kBlkBytes);
-      if (ps.extra) l2_prefetch(ps.extra + (int64_t)Q * BLK, kBlkBytes);
-    };
-#pragma unroll
-    for (int i = 0; i < kLook; ++i) {
-      look[i] = claim();
-      prefetch(look[i]);
-    }
     uint32_t pJ = 0;
     for (uint32_t seq = 0;; ++seq) {
-      const unsigned P = look[0];
-#pragma unroll
-      for (int i = 0; i + 1 < kLook; ++i) look[i] = look[i + 1];
-      look[kLook - 1] = P == kEndBlock ? kEndBlock : claim();
-      prefetch(look[kLook - 1]);
+      const unsigned P = claim();
       unsigned prem = P == kEndBlock ? 0u : (P & nbmask);
       // jobs of P: [the partial-sum block,] neighbours (far bits first), the
       // own block.  The DRAM-sourced partial sums go first so their load can
       // start in a slot freed during the previous block's epilogue.
-      int stage = (ps.extra && tuning_extra_first) ? 1 : (prem ? 0 : (ps.extra ? 1 : (OWN ? 2 : 3)));
+      int stage = ps.extra ? 1 : (prem ? 0 : (OWN ? 2 : 3));
       for (bool first = true;; first = false) {
         const int slot = pJ % kRing;
         if (pJ >= kRing) mbar_wait(&sm.empty[slot], ((pJ / kRing) - 1) & 1u);
-        if (first) blkq[seq % kBlkQ] = P;          // published by the arrive below
+        if (first) {                               // published by the arrive below
+          blkq[seq % kBlkQ] = P;
+          blkc[seq % kBlkQ] = c;
+        }
         if (P == kEndBlock) {
           mbar_arrive(&sm.full[slot]);             // tx-free arrival: the end marker
           return;
@@ -763,11 +712,10 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
           const int j = 31 - __clz(prem);
           prem &= ~(1u << j);
           srcp = table + (int64_t)(P ^ (1u << j)) * BLK;
-          pol = j >= near_bits ? pol_far : pol_near;
-          if (!prem) stage = (ps.extra && !tuning_extra_first) ? 1 : (OWN ? 2 : 4);
+          if (!prem) stage = OWN ? 2 : 4;
         } else if (stage == 1) {
           srcp = ps.extra + (int64_t)P * BLK;
-          stage = tuning_extra_first ? (prem ? 0 : (OWN ? 2 : 4)) : (OWN ? 2 : 4);
+          stage = prem ? 0 : (OWN ? 2 : 4);
         } else if (stage == 2) {
           srcp = table + (int64_t)P * BLK;
           pol = pol_own;
@@ -807,6 +755,7 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
     mbar_wait(&sm.full[J % kRing], (J / kRing) & 1u);   // first job of the block (or the end)
     const unsigned Pg = *(volatile unsigned *)&blkq[seq % kBlkQ];
     if (Pg == kEndBlock) break;
+    const int64_t lrow0 = (int64_t)(*(volatile unsigned *)&blkc[seq % kBlkQ]) * BLK;
     // stacked multi-dataset launch: block Pg of the stack is block P of
     // dataset d + (Pg >> nP) (one dataset: Pg = P)
     const unsigned P = Pg & ((1u << nP) - 1u);
@@ -954,8 +903,8 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
       const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
       const int64_t b0 = sm.base[buf][q];
       const int k = kP + q;
-      const int64_t row = b0 + t;
-      const bool valid = b0 != kNoRun && row >= 0 && row < rows;
+      const int64_t row = ps.local ? lrow0 + tid + kStencilThreads * r : b0 + t;
+      const bool valid = b0 != kNoRun && (ps.local || (row >= 0 && row < rows));
       double tc = 0.0, dtc = 0.0, o = 0.0;
       if (valid) {
         const double l = own[swz(e)], nb = nbs[swz(e)];
@@ -1010,215 +959,217 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
   }
 }
 
-// ---------------------------------------------------------------------------
-// Fused engine-2 pass: one persistent warp per CTA claims table blocks in
-// increasing index order, PRODUCES T[P] (Schur elimination of P's prefix
-// variables + the register leaf recursion), publishes it (release flag),
-// then CONSUMES P: every neighbour block P ^ (1<<j) has a smaller index, so
-// it was claimed earlier by a running CTA whose production never waits --
-// the acquire-wait always terminates.  The own block never round-trips
-// through HBM and the FP64 table work overlaps the output stream.
-// ---------------------------------------------------------------------------
-__device__ double2 g_logtab[256];
+// Full-output stencil with the own block OUTSIDE the ring (the round-2
+// pass-2 kernel).  In k_lattice_measures<MODE_FULL> the own block is the
+// last job of a block's in-order ring and stays in its slot through the
+// run-ordered epilogue, so the next block's later jobs cannot be issued
+// until the epilogue ends and their L2/DRAM latency is exposed once per
+// block (ncu, round 1: consumer warps spent ~30% of their issue slots
+// polling ring barriers).  Here the producer loads each block's own T[P]
+// FIRST, into a double-buffered own area with its own full/empty
+// mbarriers (released after the epilogue), and the ring carries only the
+// partial-sum and neighbour jobs, which are released as soon as they are
+// accumulated.  One neighbour-sum buffer (a second named barrier keeps the
+// next block's nbs writes behind this block's epilogue reads) keeps the
+// CTA at 53 KB of shared memory: 4 CTAs per SM.
+constexpr int kRingOwn = 3;
 
-constexpr long long kSpinLimit = 20000000000ll;   // ~10 s at 2 GHz: fail loudly, never hang
+struct FullSmem {
+  double ring[kRingOwn][BLK];
+  double own[2][BLK];
+  double nbs[BLK];
+  uint32_t run[BLK];
+  uint64_t full[kRingOwn];
+  uint64_t empty[kRingOwn];
+  uint64_t own_full[2];
+  uint64_t own_empty[2];
+  int64_t base[2][CB + 1];
+};
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(32)
-k_lattice_fused(const double *__restrict__ corr, int N, int D, int d, int kmin, int kmax,
-                const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
-                int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
-                double *__restrict__ table, unsigned *__restrict__ flags,
-                unsigned *__restrict__ counter, int *__restrict__ err) {
-  __shared__ __align__(16) double own[BLK];
-  __shared__ __align__(16) double nbs[BLK];       // also the gathered matrix while producing
-  __shared__ int vars[MAXV];
-  __shared__ int64_t s_base[CB + 1];
-  const int lane = threadIdx.x;
+__global__ void __launch_bounds__(kStencilThreads + 32, 4)
+k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
+               const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
+               int64_t g_begin, int64_t g_end, double *__restrict__ out, int64_t plane,
+               unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
+               unsigned *__restrict__ counter, StencilPass ps) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  FullSmem &sm = *reinterpret_cast<FullSmem *>(smem_raw);
+  __shared__ unsigned blkq[kBlkQ];
+  __shared__ unsigned blkc[kBlkQ];
+  constexpr uint32_t kBlkBytes = BLK * sizeof(double);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int p = tid; p < BLK; p += blockDim.x) {
+    const int e = __ldg(g_runmask + p);
+    const int q = __popc(e);
+    sm.run[p] = (uint32_t)e | ((uint32_t)(p - c_runstart[q]) << 10) | ((uint32_t)q << 20);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kRingOwn; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.own_full[b], 1);
+      mbar_init(&sm.own_empty[b], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const unsigned nbmask = ps.nbmask;
   const int nP = N - CB;
-  const unsigned nblocks = 1u << nP;
-  const double2 *logtab = g_logtab;
-  const int near_bits = nP > kFarBits + kMinNearBits ? nP - kFarBits : nP;
-  for (;;) {
-    unsigned P = 0;
-    if (lane == 0) P = atomicAdd(counter, 1u);
-    P = __shfl_sync(0xffffffffu, P, 0);
-    if (P >= nblocks) break;
-    // ------------------------------------------------ produce T[P] ----
-    const int nfix = __popc(P);
-    const int m = nfix + CB;
-    if (lane == 0) {
-      int nf = 0;
-      for (int j = 0; j < nP; ++j)
-        if ((P >> j) & 1) vars[nf++] = j;
-      for (int t = 0; t < CB; ++t) vars[nf + t] = nP + t;
-    }
-    __syncwarp();
-    double *M = nbs;                                  // m <= 32 -> m*m <= 1024
-    if (lane < m) {
-      const int vl = vars[lane];
-      for (int i = 0; i < m; ++i)
-        M[i * m + lane] = __ldg(corr + ((int64_t)vars[i] * N + vl) * D + d);
-    }
-    __syncwarp();
-    double m0 = 1.0;
-    int e0 = 0;
-    int bad = 0;
-    for (int j = 0; j < nfix; ++j) {
-      const double p = M[j * m + j];
-      bad |= !(p > kMinPivot);
-      lp_mul(m0, e0, p);
-      const double rp = 1.0 / p;
-      // lane = column: row j's entry stays in a register, column j is a
-      // broadcast read, the lane's own column is conflict-free
-      if (lane > j && lane < m) {
-        const double mj = M[j * m + lane] * rp;
-        for (int i = j + 1; i < m; ++i) M[i * m + lane] = fma(-M[i * m + j], mj, M[i * m + lane]);
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------ producer ----
+    if (lane != 0) return;
+    const uint64_t pol_near = l2_policy(false), pol_own = l2_policy_last();
+    const int hb = nP - ps.perm_lb;
+    unsigned c = 0;
+    auto claim = [&]() -> unsigned {
+      if (ps.list) {
+        c = atomicAdd(counter, 1u);
+        return c < *ps.nlist ? ps.list[c] : kEndBlock;
       }
-      __syncwarp();
-    }
-    double c[CB * (CB + 1) / 2];
-#pragma unroll
-    for (int i = 0; i < CB; ++i)
-#pragma unroll
-      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = M[(nfix + i) * m + (nfix + l)];
-    double ml = m0;
-    int el = e0;
-#pragma unroll
-    for (int j = 0; j < LANE_BITS; ++j) {
-      const bool inc = (lane >> j) & 1;
-      const double p = c[j * (j + 1) / 2 + j];
-      if (inc && !(p > kMinPivot)) bad = 1;
-      const double f = inc ? 1.0 / p : 0.0;
-      if (inc) lp_mul(ml, el, p);
-#pragma unroll
-      for (int i = j + 1; i < CB; ++i) {
-        const double ci = c[i * (i + 1) / 2 + j] * f;
-#pragma unroll
-        for (int l = j + 1; l <= i; ++l)
-          c[i * (i + 1) / 2 + l] = fma(-ci, c[l * (l + 1) / 2 + j], c[i * (i + 1) / 2 + l]);
-      }
-    }
-    {
-      int ex;
-      ml = frexp(ml, &ex);
-      el += ex;
-    }
-    constexpr int R = CB - LANE_BITS;
-    double a[R * (R + 1) / 2];
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int l = 0; l <= i; ++l)
-        a[i * (i + 1) / 2 + l] = c[(i + LANE_BITS) * (i + LANE_BITS + 1) / 2 + (l + LANE_BITS)];
-    Leaf<R, true>::run(a, ml, el, 0, own, lane, bad, logtab);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
-    __syncwarp();
-    // publish: table block to HBM (kept in L2 for the near consumers)
-    {
-      double *tp = table + (int64_t)P * BLK;
-#pragma unroll 8
-      for (int x = 0; x < BLK / 32; ++x) __stcg(tp + 32 * x + lane, own[32 * x + lane]);
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(flags + P, 1u);
-    // ------------------------------------------------ consume P ------
-    // lane owns entries e = 32 x + lane, x = 0..31
-    double acc[BLK / 32];
-#pragma unroll
-    for (int x = 0; x < BLK / 32; ++x) acc[x] = 0.0;
-    uint32_t rem = P;
-    while (rem) {
-      const int j = 31 - __clz(rem);                 // far (high) bits first
-      rem &= ~(1u << j);
-      const unsigned Pn = P ^ (1u << j);
-      if (lane == 0) {
-        long long t0 = clock64();
-        while (ld_acquire(flags + Pn) == 0u) {
-          if (clock64() - t0 > kSpinLimit) {
-            atomicExch(err, 2);
-            break;
-          }
+      for (;;) {
+        c = atomicAdd(counter, 1u);
+        if (c >= blk_end - blk_begin) return kEndBlock;
+        if (ps.nstack > 0) {                       // see k_lattice_measures
+          const unsigned dl = ((c >> (2 + nP)) << 2) | (c & 3u);
+          if (dl >= ps.nstack) continue;
+          return (dl << nP) | ((c >> 2) & ((1u << nP) - 1u));
         }
+        const unsigned q = ps.perm_lb ? (((c & ((1u << hb) - 1u)) << ps.perm_lb) | (c >> hb)) : c;
+        if (!active || active[blk_begin + q]) return blk_begin + q;
       }
-      __syncwarp();
-      const double *nb = table + (int64_t)Pn * BLK;
-      if (j >= near_bits) {
-#pragma unroll
-        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcs(nb + swz(32 * x + lane));
-      } else {
-#pragma unroll
-        for (int x = 0; x < BLK / 32; ++x) acc[x] += __ldcg(nb + swz(32 * x + lane));
+    };
+    uint32_t pJ = 0;
+    for (uint32_t seq = 0;; ++seq) {
+      const unsigned Pg = claim();
+      const int ob = seq & 1;
+      if (seq >= 2) mbar_wait(&sm.own_empty[ob], ((seq >> 1) - 1) & 1u);
+      blkq[seq % kBlkQ] = Pg;                      // published by the own-block arrival
+      blkc[seq % kBlkQ] = c;
+      if (Pg == kEndBlock) {
+        mbar_arrive(&sm.own_full[ob]);             // tx-free arrival: the end marker
+        return;
       }
-    }
-    // lexicographic base rank of each run
-    const int kP = nfix;
-    if (lane <= CB) {
-      const int q = lane, k = kP + q;
-      int64_t base = -1;
-      if (k >= kmin && k <= kmax && k >= 1) {
-        uint64_t r = binom_g(N, k) - 1;
-        int i = 0;
-        for (int j = 0; j < nP; ++j)
-          if ((P >> j) & 1) r -= binom_g(N - 1 - j, k - i++);
-        for (int t = 0; t < q; ++t) r -= binom_g(N - 1 - (nP + t), k - i++);
-        base = order_off[k - kmin] + (int64_t)r - g_begin;
-      }
-      s_base[q] = base;
-    }
-#pragma unroll
-    for (int x = 0; x < BLK / 32; ++x) {
-      const int e = 32 * x + lane;
-      double s = acc[x];
-#pragma unroll
-      for (int t = 0; t < CB; ++t)
-        if ((e >> t) & 1) s += own[swz(e ^ (1 << t))];
-      nbs[swz(e)] = s;
-    }
-    __syncwarp();
-    const double *et = eta ? eta + (int64_t)d * kstride : nullptr;
-    const double e1 = et ? et[1] : 0.0;
-    for (int q = 0; q <= CB; ++q) {
-      const int k = kP + q;
-      if (k < kmin || k > kmax || k < 1) continue;
-      const int64_t b0 = s_base[q];
-      const int len = (int)binom(CB, q);
-      const int start = c_runstart[q];
-      const double kd = (double)k;
-      const double ek = et ? et[k] : 0.0, ek1 = et ? et[k - 1] : 0.0;
-      for (int t = lane; t < len; t += 32) {
-        const int64_t row = b0 + t;
-        if (row < 0 || row >= g_end - g_begin) continue;
-        const int e = __ldg(g_runmask + start + t);
-        const double l = own[swz(e)], nb = nbs[swz(e)];
-        double tc, dtc, o;
-        if (et) {
-          tc = -0.5 * l - kd * e1 + ek;
-          dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
-          o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+      const unsigned dl = Pg >> nP, P = Pg & ((1u << nP) - 1u);
+      const double *tab = table + ((int64_t)dl << N);
+      mbar_expect_tx(&sm.own_full[ob], kBlkBytes);
+      tma_load_1d(sm.own[ob], tab + (int64_t)P * BLK, kBlkBytes, &sm.own_full[ob], pol_own);
+      unsigned prem = P & nbmask;
+      bool extra = ps.extra != nullptr;
+      while (extra || prem) {
+        const int slot = pJ % kRingOwn;
+        if (pJ >= kRingOwn) mbar_wait(&sm.empty[slot], ((pJ / kRingOwn) - 1) & 1u);
+        const double *srcp;
+        if (extra) {                               // DRAM-sourced: first
+          srcp = ps.extra + (int64_t)P * BLK;
+          extra = false;
         } else {
-          tc = -0.5 * l;
-          dtc = 0.5 * ((1.0 - kd) * l + nb);
-          o = 0.5 * ((kd - 2.0) * l - nb);
+          const int j = 31 - __clz(prem);          // far bits first
+          prem &= ~(1u << j);
+          srcp = tab + (int64_t)(P ^ (1u << j)) * BLK;
         }
-        const int64_t oi = row * D + d;
-        __stcs(out + oi, tc);
-        __stcs(out + plane + oi, dtc);
-        __stcs(out + 2 * plane + oi, o);
-        __stcs(out + 3 * plane + oi, tc + dtc);
+        mbar_expect_tx(&sm.full[slot], kBlkBytes);
+        tma_load_1d(sm.ring[slot], srcp, kBlkBytes, &sm.full[slot], pol_near);
+        ++pJ;
       }
     }
-    __syncwarp();
+  }
+
+  // -------------------------------------------------------- consumers ----
+  const int64_t rows = g_end - g_begin;
+  constexpr int PAIRS = PER / 2;
+  int pw[PAIRS];
+  bool flip[PAIRS];
+#pragma unroll
+  for (int r = 0; r < PAIRS; ++r) {
+    const int e = 2 * (tid + kStencilThreads * r);
+    pw[r] = swz(e) & ~1;
+    flip[r] = (e >> 5) & 1;
+  }
+  uint32_t J = 0;
+  for (uint32_t seq = 0;; ++seq) {
+    const int buf = seq & 1;
+    mbar_wait(&sm.own_full[buf], (seq >> 1) & 1u);
+    const unsigned Pg = *(volatile unsigned *)&blkq[seq % kBlkQ];
+    if (Pg == kEndBlock) break;
+    const int64_t lrow0 = (int64_t)(*(volatile unsigned *)&blkc[seq % kBlkQ]) * BLK;
+    const unsigned P = Pg & ((1u << nP) - 1u);
+    const int dd = d + (int)(Pg >> nP);
+    const double *et = eta ? eta + (int64_t)dd * kstride : nullptr;
+    const double e1 = et ? et[1] : 0.0;
+    const int kP = __popc(P);
+    const int nj = __popc(P & nbmask) + (ps.extra ? 1 : 0);
+    if (tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
+    double2 acc[PAIRS];
+#pragma unroll
+    for (int r = 0; r < PAIRS; ++r) acc[r] = make_double2(0.0, 0.0);
+    for (int m = 0; m < nj; ++m, ++J) {
+      const int slot = J % kRingOwn;
+      mbar_wait(&sm.full[slot], (J / kRingOwn) & 1u);
+      const double *src = sm.ring[slot];
+#pragma unroll
+      for (int r = 0; r < PAIRS; ++r) {
+        const double2 v = *reinterpret_cast<const double2 *>(src + pw[r]);
+        acc[r].x += v.x;
+        acc[r].y += v.y;
+      }
+      release_slot(&sm.empty[slot], lane);
+    }
+    const double *own = sm.own[buf];
+    if (seq > 0) named_bar_sync(2, kStencilThreads);   // previous epilogue done with nbs
+#pragma unroll
+    for (int r = 0; r < PAIRS; ++r) {
+      const int e0 = 2 * (tid + kStencilThreads * r);
+      const double2 ov = *reinterpret_cast<const double2 *>(own + pw[r]);
+      const double o0 = flip[r] ? ov.y : ov.x;
+      double s0 = flip[r] ? acc[r].y : acc[r].x;
+      double s1 = (flip[r] ? acc[r].x : acc[r].y) + o0;   // bit-0 neighbour of e0+1 is e0
+#pragma unroll
+      for (int t = 1; t < CB; ++t) {
+        if ((e0 >> t) & 1) {
+          const int n0 = e0 ^ (1 << t);
+          const double2 v = *reinterpret_cast<const double2 *>(own + (swz(n0) & ~1));
+          const bool f = (n0 >> 5) & 1;
+          s0 += f ? v.y : v.x;
+          s1 += f ? v.x : v.y;
+        }
+      }
+      *reinterpret_cast<double2 *>(sm.nbs + pw[r]) = flip[r] ? make_double2(s1, s0) : make_double2(s0, s1);
+    }
+    named_bar_sync(1, kStencilThreads);           // nbs and base[buf] complete
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t w = sm.run[tid + kStencilThreads * r];
+      const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
+      const int64_t b0 = sm.base[buf][q];
+      const int k = kP + q;
+      const int64_t row = ps.local ? lrow0 + tid + kStencilThreads * r : b0 + t;
+      const bool valid = b0 != kNoRun && (ps.local || (row >= 0 && row < rows));
+      if (!valid) continue;
+      const double l = own[swz(e)], nb = sm.nbs[swz(e)];
+      const double kd = (double)k;
+      double tc, dtc, o;
+      if (et) {
+        const double ek = et[k], ek1 = et[k - 1];
+        tc = -0.5 * l - kd * e1 + ek;
+        dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
+        o = 0.5 * ((kd - 2.0) * l - nb) - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+      } else {
+        tc = -0.5 * l;
+        dtc = 0.5 * ((1.0 - kd) * l + nb);
+        o = 0.5 * ((kd - 2.0) * l - nb);
+      }
+      // streaming (evict-first) stores: the 32 B/n-plet output must not
+      // push the log-det table's neighbour blocks out of L2
+      const int64_t oi = row * D + dd;
+      __stcs(out + oi, tc);
+      __stcs(out + plane + oi, dtc);
+      __stcs(out + 2 * plane + oi, o);
+      __stcs(out + 3 * plane + oi, tc + dtc);
+    }
+    release_slot(&sm.own_empty[buf], lane);       // own block free for block seq + 2
   }
 }
 
@@ -1262,7 +1213,6 @@ void upload_tables() {
     lt[j].y = (double)(-logl((long double)cd));
   }
   cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * 256);
-  cudaMemcpyToSymbol(g_logtab, lt.data(), sizeof(double2) * 256);
   cudaMemcpyToSymbol(g_runmask, rm.data(), sizeof(uint16_t) * BLK);
   {
     std::vector<uint32_t> gr(BLK);
@@ -1370,46 +1320,6 @@ static LatticeWs ws_view(void *ws, int N) {
   return w;
 }
 
-int lattice_fused(const double *corr, int N, int D, int d, const double *eta, int kstride,
-                  int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, void *ws,
-                  size_t ws_bytes, cudaStream_t s) {
-  size_t need = 0;
-  int st = lattice_ws_bytes(N, D, &need);
-  if (st) return st;
-  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
-  upload_binomials();
-  upload_tables();
-  LatticeWs w = ws_view(ws, N);
-  const int nP = N - CB;
-  int64_t h_off[MAXV + 1];
-  int64_t acc = 0;
-  for (int k = kmin; k <= kmax; ++k) {
-    h_off[k - kmin] = acc;
-    acc += (int64_t)host_binom(N, k);
-  }
-  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(w.ready, 0, sizeof(unsigned) << nP, s);
-  cudaMemsetAsync(w.flag, 0, 64, s);
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_fused, 32, 0);
-  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  if (grid > (1ll << nP)) grid = 1ll << nP;
-  const int64_t plane = (g_end - g_begin) * (int64_t)D;
-  k_lattice_fused<<<(unsigned)grid, 32, 0, s>>>(corr, N, D, d, kmin, kmax, eta, kstride, w.offs,
-                                                g_begin, g_end, out, plane, w.table, w.ready,
-                                                w.counter, w.err);
-  if ((st = check_launch("k_lattice_fused"))) return st;
-  int h_err = 0;
-  cudaMemcpyAsync(&h_err, w.err, sizeof(int), cudaMemcpyDeviceToHost, s);
-  cudaStreamSynchronize(s);
-  if (h_err == 1) return fail(HOI_FALLBACK, "lattice: correlation matrix not numerically positive "
-                                            "definite; rerun with the per-n-plet engine");
-  if (h_err) return fail(HOI_CUDA_ERROR, "lattice: fused pass timed out waiting for a block");
-  return HOI_OK;
-}
-
 int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_bytes,
                   cudaStream_t s, bool reset_flag = true) {
   size_t need = 0;
@@ -1425,11 +1335,6 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   return check_launch("k_lattice_table");
 }
 
-// Neighbour reads beyond this bit use evict-first loads.  Measured on B200
-// (cfg4, persistent stencil): marking any neighbour evict-first costs time
-// (17.1 ms with none vs 17.8 ms with the top 6 bits), so none is marked.
-static int default_near_bits(int nP) { return nP; }
-
 static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   int64_t acc = 0;
   for (int k = kmin; k <= kmax; ++k) {
@@ -1443,10 +1348,9 @@ template <int R, int C, int F, int NB = 2>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
                        int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
-                       int near_bits, int own_last, int per_sm_cap, const StencilFilter &flt,
-                       const StencilPass &ps, cudaStream_t s) {
+                       const StencilFilter &flt, const StencilPass &ps, cudaStream_t s) {
   static thread_local int set_for = -1;
-  static thread_local int grid_cap = 0, n_sms = 0, max_per_sm = 0;
+  static thread_local int grid_cap = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   const int smem = (int)sizeof(StencilSmem<R, NB>);
@@ -1456,31 +1360,56 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_measures<R, C, F, NB>,
                                                   kStencilThreads + 32, smem);
-    max_per_sm = per_sm > 0 ? per_sm : 1;
-    n_sms = sms;
-    grid_cap = sms * max_per_sm;
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     set_for = dev;
   }
   const unsigned n = blk_end - blk_begin;
-  unsigned cap = (unsigned)grid_cap;
-  if (per_sm_cap > 0 && per_sm_cap < max_per_sm) cap = (unsigned)(n_sms * per_sm_cap);
-  const unsigned grid = n < cap ? n : cap;
+  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
   if (grid == 0) return HOI_OK;
   k_lattice_measures<R, C, F, NB><<<grid, kStencilThreads + 32, smem, s>>>(
       w.table, N, D, d, kmin, kmax, eta, kstride, w.offs, g_begin, g_end, out, plane, blk_begin,
-      blk_end, active, near_bits, w.counter, own_last, flt, ps);
+      blk_end, active, w.counter, flt, ps);
   return check_launch("k_lattice_measures");
+}
+
+static int run_full(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
+                    int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, int64_t plane,
+                    unsigned blk_begin, unsigned blk_end, const uint8_t *active,
+                    const StencilPass &ps, cudaStream_t s) {
+  static thread_local int set_for = -1;
+  static thread_local int grid_cap = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int smem = (int)sizeof(FullSmem);
+  if (set_for != dev) {
+    cudaFuncSetAttribute(k_lattice_full, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_full, kStencilThreads + 32,
+                                                  smem);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    set_for = dev;
+  }
+  const unsigned n = blk_end - blk_begin;
+  const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
+  if (grid == 0) return HOI_OK;
+  k_lattice_full<<<grid, kStencilThreads + 32, smem, s>>>(w.table, N, D, d, kmin, kmax, eta,
+                                                          kstride, w.offs, g_begin, g_end, out,
+                                                          plane, blk_begin, blk_end, active,
+                                                          w.counter, ps);
+  return check_launch("k_lattice_full");
 }
 
 // Persistent stencil launch over table blocks [blk_begin, blk_end): one
 // CTA per resident slot (SMs x occupancy).  For a partial rank range the
 // blocks without output are flagged first (one thread per block) and
-// skipped without streaming them.
+// skipped without streaming them.  local: write block-major local rows
+// (the compacted list's claim order; see StencilPass::local).
 static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                           int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
-                          unsigned blk_begin, unsigned blk_end, int near_bits, bool partial,
-                          bool flags_ready, cudaStream_t s, int per_sm_cap = 0,
-                          const StencilFilter *flt = nullptr) {
+                          unsigned blk_begin, unsigned blk_end, bool partial, bool flags_ready,
+                          cudaStream_t s, const StencilFilter *flt = nullptr,
+                          int64_t local_rows = 0) {
   const unsigned nblocks = 1u << (N - CB);
   uint8_t *active = partial ? reinterpret_cast<uint8_t *>(w.ready) : nullptr;
   if (partial && !flags_ready) {
@@ -1489,13 +1418,7 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     int st = check_launch("k_block_active");
     if (st) return st;
   }
-  // measured on B200 (cfg4): 4 CTAs x 4-slot rings beat 3 x 6 (17.8 ms) and
-  // 2 x 10 (20.7 ms) -- more independent in-order streams per SM; own block
-  // evict_last (tuning(), top of file)
-  const int ring = tuning().ring;
-  const int own_last = tuning().own_last;
-  if (tuning().near_bits >= 0) near_bits = tuning().near_bits;
-  const int64_t plane = (g_end - g_begin) * (int64_t)D;
+  const int64_t plane = (local_rows ? local_rows : g_end - g_begin) * (int64_t)D;
   const int nP = N - CB;
   const unsigned all = (1u << nP) - 1u;
   // Two-pass split over the whole block space (nP >= 14): pass 1 writes the
@@ -1509,20 +1432,15 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   // (DRAM 68.8 vs 84.2 GB); the filtered (TopK) pass writes nothing and is
   // bound by per-job TMA latency rather than bytes, so there the single pass
   // wins (11.4 ms vs 3.4 + 9.6 ms).
-  const int two_env = tuning().two_pass;
-  const int two_flt = tuning().two_pass_filter;
-  const bool two = (flt ? two_flt : two_env) && nP >= 14 && blk_begin == 0 &&
-                   blk_end == (1u << nP) && w.lowsum;
+  const bool two = !flt && nP >= 14 && blk_begin == 0 && blk_end == (1u << nP) && w.lowsum;
   const int lb = nP / 2;
   const StencilFilter none{};
-  // claim-ahead L2 prefetch of the own / pass-1-sum blocks: measured no
-  // gain on B200 (cfg4 19.75-19.89 ms with vs 19.16 without), off
-  const int pf = tuning().prefetch;
-  StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr, pf};
+  StencilPass ps{all, nullptr, nullptr, 0, nullptr, nullptr, 0u, local_rows ? 1 : 0};
   // partial / sampled scans over the whole block space: compacted block
   // lists (natural order for a single pass or pass 1, high-bits-fastest for
   // pass 2) in the workspace after the flags
   const bool listed = active && blk_begin == 0 && blk_end == (1u << nP);
+  if (local_rows && !listed) return fail(HOI_INVALID_ARG, "lattice: local rows need a block list");
   unsigned *list1 = w.list, *list2 = w.list + (1u << nP), *cnts = w.list + 2 * (1u << nP);
   if (listed) {
     const unsigned ntiles = ((1u << nP) + kCompactTile - 1) / kCompactTile;
@@ -1539,51 +1457,26 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
     ps.nlist = cnts;
   }
   if (two) {
-    StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0};
-    cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
     // the low pass stores its sums straight from registers: no neighbour-sum
     // buffer or run table, so 6 ring slots fit at 4 CTAs/SM
-    int st = tuning().lowsum_ring6
-                 ? run_stencil<6, 4, MODE_LOWSUM, 0>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
-                                                     g_end, out, plane, blk_begin, blk_end, active,
-                                                     near_bits, own_last, per_sm_cap, none, p1, s)
-             : ring == 5
-                 ? run_stencil<5, 4, MODE_LOWSUM, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
-                                                     g_end, out, plane, blk_begin, blk_end, active,
-                                                     near_bits, own_last, per_sm_cap, none, p1, s)
-                 : run_stencil<4, 4, MODE_LOWSUM>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
-                                                  g_end, out, plane, blk_begin, blk_end, active,
-                                                  near_bits, own_last, per_sm_cap, none, p1, s);
+    const StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0u, 0};
+    cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+    int st = run_stencil<kRingLean, 4, MODE_LOWSUM, 0>(w, N, D, d, eta, kstride, kmin, kmax,
+                                                       g_begin, g_end, out, plane, blk_begin,
+                                                       blk_end, active, none, p1, s);
     if (st) return st;
     ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
-                     listed ? cnts + 1 : nullptr, pf, 0u, tuning().extra_first};
+                     listed ? cnts + 1 : nullptr, 0u, local_rows ? 1 : 0};
   }
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
   // Filter mode finishes entries from registers (no neighbour-sum buffer),
   // so 6 ring slots fit at 4 CTAs/SM: 24 TMA jobs in flight per SM, not 16.
-  if (flt && tuning().filter_ring6)
-    return run_stencil<6, 4, MODE_FILTER, 0>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
-                                             g_end, out, plane, blk_begin, blk_end, active,
-                                             near_bits, own_last, per_sm_cap, *flt, ps, s);
-  if (flt && ring == 5)
-    return run_stencil<5, 4, MODE_FILTER, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin,
-                                             g_end, out, plane, blk_begin, blk_end, active,
-                                             near_bits, own_last, per_sm_cap, *flt, ps, s);
   if (flt)
-    return run_stencil<4, 4, MODE_FILTER>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
-                                          out, plane, blk_begin, blk_end, active, near_bits,
-                                          own_last, per_sm_cap, *flt, ps, s);
-  if (ring == 5)
-    return run_stencil<5, 4, MODE_FULL, 1>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end,
-                                           out, plane, blk_begin, blk_end, active, near_bits,
-                                           own_last, per_sm_cap, none, ps, s);
-  if (ring == 6)
-    return run_stencil<6, 3, MODE_FULL>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
-                                        plane, blk_begin, blk_end, active, near_bits, own_last,
-                                        per_sm_cap, none, ps, s);
-  return run_stencil<4, 4, MODE_FULL>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out,
-                                      plane, blk_begin, blk_end, active, near_bits, own_last,
-                                      per_sm_cap, none, ps, s);
+    return run_stencil<kRingLean, 4, MODE_FILTER, 0>(w, N, D, d, eta, kstride, kmin, kmax,
+                                                     g_begin, g_end, out, plane, blk_begin,
+                                                     blk_end, active, *flt, ps, s);
+  return run_full(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane, blk_begin,
+                  blk_end, active, ps, s);
 }
 
 int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstride, int kmin,
@@ -1596,7 +1489,7 @@ int lattice_measures(void *ws, int N, int D, int d, const double *eta, int kstri
   cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
   const bool partial = g_begin > 0 || g_end < total;
   return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, 0u,
-                        1u << (N - CB), default_near_bits(N - CB), partial, false, s);
+                        1u << (N - CB), partial, false, s);
 }
 
 // Filtered stencil over the whole rank space of [kmin, kmax] (or every
@@ -1621,7 +1514,7 @@ int lattice_filter(void *ws, int N, int D, int d, const double *eta, int kstride
   }
   StencilFilter f{m_idx, sign, key_max, cand, count, cand_cap};
   return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, nullptr, 0u, nblocks,
-                        default_near_bits(N - CB), sampled, sampled, s, 0, &f);
+                        sampled, sampled, s, &f);
 }
 
 // Block-sharded scan (multi-GPU): shard `shard` of 2^sb owns the table
@@ -1643,15 +1536,17 @@ int lattice_status(void *ws, int N, cudaStream_t s);
 int lattice_shard(const double *corr, int N, int D, int d, const double *eta, int kstride,
                   int kmin, int kmax, unsigned long long mask, int sb, unsigned every,
                   double *out, const StencilFilter *flt, bool build, void *ws, size_t ws_bytes,
-                  cudaStream_t s) {
+                  cudaStream_t s, int64_t local_rows = 0) {
   size_t need = 0;
   int st = lattice_ws_bytes(N, D, &need);
   if (st) return st;
   if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
   const int nP = N - CB;
-  if (sb < 0 || sb > nP / 2 || sb > 6 || mask == 0 || (sb < 6 && (mask >> (1 << sb)) != 0))
-    return fail(HOI_INVALID_ARG,
-                "lattice_shard: need a non-empty shard mask below 2^(2^sb), sb <= min(6, (N-10)/2)");
+  const int bexp = nP < MAXB ? nP : MAXB;        // prefix variables a table CTA expands
+  if (sb < 0 || sb > nP / 2 || sb > 6 || sb > nP - bexp || mask == 0 ||
+      (sb < 6 && (mask >> (1 << sb)) != 0))
+    return fail(HOI_INVALID_ARG, "lattice_shard: need a non-empty shard mask below 2^(2^sb), "
+                                 "sb <= min(6, (N-10)/2, N-16)");
   upload_binomials();
   upload_tables();
   LatticeWs w = ws_view(ws, N);
@@ -1675,75 +1570,53 @@ int lattice_shard(const double *corr, int N, int D, int d, const double *eta, in
   k_block_shard<<<(nblocks + 255) / 256, 256, 0, s>>>(nblocks, nP, sb, mask, every,
                                                       reinterpret_cast<uint8_t *>(w.ready));
   if ((st = check_launch("k_block_shard"))) return st;
-  return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, out, 0u, nblocks,
-                        default_near_bits(nP), true, true, s, 0, flt);
+  return launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, 0, total, out, 0u, nblocks, true,
+                        true, s, flt, local_rows);
 }
 
-// Two-stream pipeline over chunks of 2^w table blocks: the table of chunk
-// c+1 is built on an auxiliary stream while the stencil consumes chunk c,
-// so a chunk's own blocks and its neighbours within distance 2^w (the
-// current and previous chunk, 2 x 64 MB) are read from L2 while hot, and
-// the FP64/log-bound table phase overlaps the HBM-bound stencil.
-struct PipeRes {
-  int dev = -1;
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev[1 << 10];
-  int nev = 0;
-};
-
-static PipeRes &pipe_res(int nev) {
-  static thread_local PipeRes r;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (r.dev != dev) {
-    r = PipeRes();
-    r.dev = dev;
-    cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking);
-  }
-  while (r.nev < nev) cudaEventCreateWithFlags(&r.ev[r.nev++], cudaEventDisableTiming);
-  return r;
-}
-
-int lattice_pipeline(const double *corr, int N, int D, int d, const double *eta, int kstride,
-                     int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, void *ws,
-                     size_t ws_bytes, cudaStream_t s) {
-  size_t need = 0;
-  int st = lattice_ws_bytes(N, D, &need);
-  if (st) return st;
-  if (ws_bytes < need) return fail(HOI_CAPACITY, "lattice: workspace too small");
-  upload_binomials();
-  upload_tables();
-  LatticeWs w = ws_view(ws, N);
+// The block list the last local-rows stencil claimed from (local block c =
+// list[c]): pass 2's high-bits-fastest list when the scan ran two passes.
+static void copy_local_list(const LatticeWs &w, int N, unsigned *blocks, int64_t *count,
+                            cudaStream_t s) {
   const int nP = N - CB;
-  const int b = nP < MAXB ? nP : MAXB;
-  const int wb_env = tuning().pipe_wb;
-  const int tnw = tuning().table_nw;
-  const int sper = tuning().stencil_per_sm;
-  const int wb = nP < wb_env ? nP : wb_env;         // chunk = 2^wb blocks
-  const int nchunks = 1 << (nP - wb);
-  int64_t h_off[MAXV + 1];
-  const int64_t total = total_rows(N, kmin, kmax, h_off);
-  cudaMemcpyAsync(w.offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
-  PipeRes &pr = pipe_res(nchunks + 1);
-  cudaEventRecord(pr.ev[nchunks], s);
-  cudaStreamWaitEvent(pr.aux, pr.ev[nchunks], 0);
-  const bool partial = g_begin > 0 || g_end < total;
-  const int near_bits = default_near_bits(nP);
-  const unsigned ctas = 1u << (wb - b);
-  for (int c = 0; c < nchunks; ++c) {
-    if (tnw == 8)
-      k_lattice_table<8><<<ctas, 256, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
-    else
-      k_lattice_table<4><<<ctas, 128, 0, pr.aux>>>(corr, N, D, d, b, w.table, w.flag, c * ctas);
-    if ((st = check_launch("k_lattice_table"))) return st;
-    cudaEventRecord(pr.ev[c], pr.aux);
-    cudaStreamWaitEvent(s, pr.ev[c], 0);
-    st = launch_stencil(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, (unsigned)c << wb,
-                        (unsigned)(c + 1) << wb, near_bits, partial, c > 0, s, sper);
-    if (st) return st;
+  const bool two = nP >= 14 && w.lowsum;
+  const unsigned *list = w.list + (two ? (1u << nP) : 0u);
+  const unsigned *cnt = w.list + 2 * (1u << nP) + (two ? 1 : 0);
+  cudaMemcpyAsync(blocks, list, sizeof(unsigned) << nP, cudaMemcpyDeviceToDevice, s);
+  k_count_to_i64<<<1, 1, 0, s>>>(cnt, count);
+}
+
+// Local rows -> global rows: local block c (table block P = blocks[c]) holds
+// 1024 rows in run order; row p of it is the n-plet P u Q(p) at global rank
+// run_base(P, q) + t.  Rows in [g_begin, g_end) are copied to
+// out[row - g_begin] (the 4 planes of a (rows, D) output); rows of orders
+// outside [kmin, kmax] are holes and are skipped.
+__global__ void k_local_scatter(const double *__restrict__ local, int64_t lplane,
+                                const unsigned *__restrict__ blocks, const int64_t *__restrict__ nb,
+                                int N, int D, int kmin, int kmax,
+                                const int64_t *__restrict__ order_off, int64_t g_begin,
+                                int64_t g_end, double *__restrict__ out, int64_t oplane) {
+  __shared__ int64_t base[CB + 1];
+  const int64_t n = *nb;
+  for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+    const unsigned P = blocks[c];
+    __syncthreads();
+    if (threadIdx.x <= CB) base[threadIdx.x] = run_base(P, threadIdx.x, N, kmin, kmax, order_off, g_begin);
+    __syncthreads();
+    for (int p = threadIdx.x; p < BLK; p += blockDim.x) {
+      const uint32_t wv = __ldg(g_run + p);
+      const int t = (wv >> 10) & 1023, q = wv >> 20;
+      const int64_t b0 = base[q];
+      if (b0 == kNoRun) continue;
+      const int64_t row = b0 + t;
+      if (row < 0 || row >= g_end - g_begin) continue;
+      for (int dd = 0; dd < D; ++dd) {
+        const int64_t li = (c * BLK + p) * D + dd, oi = row * D + dd;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) out[m * oplane + oi] = local[m * lplane + li];
+      }
+    }
   }
-  return HOI_OK;
 }
 
 int lattice_status(void *ws, int N, cudaStream_t s) {
@@ -1765,11 +1638,10 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
   // once after every dataset (one host sync per scan, not per dataset): a
   // failing table leaves garbage rows, and HOI_FALLBACK makes the host rerun
   // the whole scan on the per-n-plet engine with the reference's jitter rule.
-  const int pipe = tuning().pipe;
   int64_t h_off[MAXV + 1];
   const int64_t total = total_rows(N, kmin, kmax, h_off);
   const int slots = batch_slots(N, D);
-  if (!pipe && slots > 1 && g_begin == 0 && g_end == total) {
+  if (slots > 1 && g_begin == 0 && g_end == total) {
     // stacked: tables of `slots` datasets in one table launch (grid.y) and
     // one stencil launch over their 2^(N-10) x slots blocks
     upload_binomials();
@@ -1787,73 +1659,29 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
                                                                            wb.table, w.flag, 0u);
       int st = check_launch("k_lattice_table");
       if (st) return st;
-      const StencilPass ps{(1u << nP) - 1u, nullptr, nullptr, 0, nullptr, nullptr, 0,
-                           (unsigned)n};
+      const StencilPass ps{(1u << nP) - 1u, nullptr, nullptr, 0, nullptr, nullptr, (unsigned)n, 0};
       cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
       const unsigned claims = (unsigned)((n + 3) & ~3) << nP;   // 4-dataset groups
-      st = run_stencil<4, 4, MODE_FULL>(wb, N, D, d0, eta, kstride, kmin, kmax, 0, total, out,
-                                        total * (int64_t)D, 0u, claims, nullptr, nP,
-                                        tuning().own_last, 0, StencilFilter{}, ps, s);
+      st = run_full(wb, N, D, d0, eta, kstride, kmin, kmax, 0, total, out, total * (int64_t)D, 0u,
+                    claims, nullptr, ps, s);
       if (st) return st;
     }
     return lattice_status(ws, N, s);
   }
-  if (!pipe) {
-    LatticeWs w = ws_view(ws, N);
-    cudaMemsetAsync(w.flag, 0, sizeof(int), s);
-    for (int d = 0; d < D; ++d) {
-      int st = lattice_table(corr, N, D, d, ws, ws_bytes, s, false);
-      if (st) return st;
-      st = lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, s);
-      if (st) return st;
-    }
-    return lattice_status(ws, N, s);
-  }
+  LatticeWs w = ws_view(ws, N);
+  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   for (int d = 0; d < D; ++d) {
-    if (pipe) {
-      int st = lattice_pipeline(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
-                                ws_bytes, s);
-      if (st) return st;
-      st = lattice_status(ws, N, s);
-      if (st) return st;
-      continue;
-    }
-    int st = lattice_table(corr, N, D, d, ws, ws_bytes, s);
-    if (st) return st;
-    st = lattice_status(ws, N, s);      // not PD: the caller reruns with engine 1
+    int st = lattice_table(corr, N, D, d, ws, ws_bytes, s, false);
     if (st) return st;
     st = lattice_measures(ws, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, s);
     if (st) return st;
   }
-  return HOI_OK;
-}
-
-int scan_full_lattice_fused(const double *corr, const double *eta, int kstride, int N, int D,
-                            int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
-                            void *ws, size_t ws_bytes, cudaStream_t s) {
-  for (int d = 0; d < D; ++d) {
-    int st = lattice_fused(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws,
-                           ws_bytes, s);
-    if (st) return st;
-  }
-  return HOI_OK;
+  return lattice_status(ws, N, s);
 }
 
 }  // namespace hoib
 
 using namespace hoib;
-
-extern "C" int hoi_lattice_fused(const double *corr, int32_t N, int32_t D, int32_t d,
-                                 const double *eta, int32_t kstride, int32_t kmin, int32_t kmax,
-                                 int64_t g_begin, int64_t g_end, double *out, void *ws,
-                                 size_t ws_bytes, void *stream) {
-  HOI_CHECK_ARG(corr && ws && out && lattice_supports(N) && d >= 0 && d < D && kmin >= 1 &&
-                    kmin <= kmax && kmax <= N && g_begin >= 0 && g_begin <= g_end,
-                "hoi_lattice_fused: bad args");
-  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_fused: bias table too short");
-  return lattice_fused(corr, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, ws, ws_bytes,
-                       (cudaStream_t)stream);
-}
 
 extern "C" int hoi_lattice_table(const double *corr, int32_t N, int32_t D, int32_t d, void *ws,
                                  size_t ws_bytes, void *stream) {
@@ -1910,6 +1738,55 @@ extern "C" int hoi_lattice_shard_set(const double *corr, int32_t N, int32_t D, i
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_set: bias table too short");
   return lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard_mask, shard_bits, 1u, out,
                        nullptr, true, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int hoi_lattice_shard_local(const double *corr, int32_t N, int32_t D, int32_t d,
+                                       const double *eta, int32_t kstride, int32_t kmin,
+                                       int32_t kmax, uint64_t shard_mask, int32_t shard_bits,
+                                       double *out, int64_t local_rows, uint32_t *blocks,
+                                       int64_t *nblocks, void *ws, size_t ws_bytes, void *stream) {
+  HOI_CHECK_ARG(corr && ws && out && blocks && nblocks && lattice_supports(N) && d >= 0 &&
+                    d < D && kmin >= 1 && kmin <= kmax && kmax <= N && local_rows > 0,
+                "hoi_lattice_shard_local: bad args");
+  HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_lattice_shard_local: bias table too short");
+  const int sb = shard_bits;
+  HOI_CHECK_ARG(sb >= 0 && sb <= 6 && shard_mask != 0, "hoi_lattice_shard_local: bad shards");
+  const int64_t need = (int64_t)__builtin_popcountll(shard_mask) << (N - sb);
+  HOI_CHECK_ARG(local_rows >= need, "hoi_lattice_shard_local: local_rows < shard blocks x 1024");
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = lattice_shard(corr, N, D, d, eta, kstride, kmin, kmax, shard_mask, shard_bits, 1u,
+                         out, nullptr, true, ws, ws_bytes, s, local_rows);
+  if (st) return st;
+  copy_local_list(ws_view(ws, N), N, blocks, nblocks, s);
+  return check_launch("k_count_to_i64");
+}
+
+extern "C" int hoi_lattice_local_scatter(const double *local, int64_t local_rows,
+                                         const uint32_t *blocks, const int64_t *nblocks,
+                                         int32_t N, int32_t D, int32_t kmin, int32_t kmax,
+                                         int64_t g_begin, int64_t g_end, double *out,
+                                         void *stream) {
+  HOI_CHECK_ARG(local && blocks && nblocks && out && lattice_supports(N) && D >= 1 &&
+                    kmin >= 1 && kmin <= kmax && kmax <= N && g_begin >= 0 && g_begin <= g_end,
+                "hoi_lattice_local_scatter: bad args");
+  upload_binomials();
+  upload_tables();
+  int64_t h_off[MAXV + 1];
+  total_rows(N, kmin, kmax, h_off);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *offs = nullptr;
+  if (stream_alloc((void **)&offs, sizeof(h_off), s) != cudaSuccess)
+    return fail(HOI_CUDA_ERROR, "hoi_lattice_local_scatter: allocation failed");
+  cudaMemcpyAsync(offs, h_off, sizeof(int64_t) * (kmax - kmin + 1), cudaMemcpyHostToDevice, s);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_local_scatter<<<8 * sms, 256, 0, s>>>(local, local_rows * (int64_t)D, blocks, nblocks,
+                                                  N, D, kmin, kmax, offs, g_begin, g_end, out,
+                                                  (g_end - g_begin) * (int64_t)D);
+  const int st = check_launch("k_local_scatter");
+  cudaFreeAsync(offs, s);
+  return st;
 }
 
 extern "C" int hoi_lattice_shard_filter(const double *corr, int32_t N, int32_t D, int32_t d,

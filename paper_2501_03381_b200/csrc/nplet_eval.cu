@@ -9,17 +9,12 @@ namespace hoib {
 int launch_eval(const EvalArgs &A, int K, cudaStream_t s) {
   if (K < 1 || K > 64) return fail(HOI_INVALID_ARG, "order > 64 is not supported");
   int st = -1;
-  if (K <= 12) st = launch_eval_k1_12(A, K, s);
-  else if (K <= 16) st = launch_eval_k13_16(A, K, s);
-  else if (K <= 32) {
-    // 17..32: G threads per unit (registers, compile-time indices); the
-    // warp-per-unit kernel stays selectable for comparison (HOI_EVAL_WARP=1)
-    static const bool warp = [] {
-      const char *e = getenv("HOI_EVAL_WARP");
-      return e && atoi(e) != 0;
-    }();
-    st = warp ? launch_eval_warp(A, K, s) : launch_eval_group(A, K, s);
+  if (K <= 12) {
+    st = launch_eval_pipe(A, K, s);            // large-N index batches (gather-pipelined)
+    if (st < 0) st = launch_eval_k1_12(A, K, s);
   }
+  else if (K <= 16) st = launch_eval_k13_16(A, K, s);
+  else if (K <= 32) st = launch_eval_group(A, K, s);   // G threads per unit (eval_group.cu)
   return st >= 0 ? st : launch_eval_generic(A, K, s);
 }
 
@@ -111,6 +106,25 @@ extern "C" int hoi_eval_indices(const double *corr, const double *sdiag, const d
   A.N = N; A.D = D; A.mats = 0; A.idx = idx; A.idx_stride = K; A.row_map = nullptr;
   A.B = B; A.r0 = 0; A.out = out; A.plane = B * (int64_t)D; A.out_row0 = 0;
   A.logdet = logdet; A.invdiag = invdiag; A.inv_n = 0;
+  A.err_count = err_count; A.err_coords = err_coords; A.err_cap = err_cap;
+  return launch_eval(A, K, (cudaStream_t)stream);
+}
+
+extern "C" int hoi_eval_indices_into(const double *corr, const double *sdiag, const double *eta,
+                                     int32_t kstride, int32_t N, int32_t D, const int32_t *idx,
+                                     int64_t B, int32_t K, double *out, int64_t out_plane,
+                                     int32_t *err_count, int64_t *err_coords, int32_t err_cap,
+                                     void *stream) {
+  HOI_CHECK_ARG(corr && idx && out && err_count && N >= 1 && D >= 1 && B >= 0 &&
+                    out_plane >= B * (int64_t)D,
+                "hoi_eval_indices_into: bad args");
+  HOI_CHECK_ARG(K >= 1 && K <= 64 && K <= N, "hoi_eval_indices_into: bad order");
+  HOI_CHECK_ARG(!eta || kstride > K, "hoi_eval_indices_into: bias table too short");
+  EvalArgs A{};
+  A.src = corr; A.sdiag = sdiag; A.eta = eta; A.kstride = kstride;
+  A.N = N; A.D = D; A.mats = 0; A.idx = idx; A.idx_stride = K; A.row_map = nullptr;
+  A.B = B; A.r0 = 0; A.out = out; A.plane = out_plane; A.out_row0 = 0;
+  A.logdet = nullptr; A.invdiag = nullptr; A.inv_n = 0;
   A.err_count = err_count; A.err_coords = err_coords; A.err_cap = err_cap;
   return launch_eval(A, K, (cudaStream_t)stream);
 }

@@ -590,3 +590,87 @@ extern "C" int hoi_topk_filter(const double *vals, int64_t n, int32_t D, int32_t
       vals, n, D, d, sign, thresh, cand, reinterpret_cast<unsigned long long *>(cand_count), cand_cap);
   return check_launch("k_topk_filter");
 }
+
+// ------------------------------------------------- exact TopK ordering ----
+// The reference's TopK key (ref:scanner.py:75-100) is (sign * value, index
+// tuple), ascending: one CTA per dataset sorts that dataset's candidate
+// positions (hoi_topk_select_multi's output: the k best keys plus every tie
+// at the k-th) by the orderable 64-bit key, equal keys by the lexicographic
+// index tuple of their rows (idx, (n, K) int32: a fixed-order batch, so
+// tuples have equal length), equal tuples by position (a stable sort of the
+// batch order), and writes the first min(k, count) positions.  Bitonic sort
+// over a power-of-two padding in shared memory; the tuple comparison only
+// runs on exactly equal keys.
+constexpr int kOrderMax = 8192;          // candidates per dataset (128 KB of smem)
+constexpr int kOrderThreads = 1024;
+
+__device__ __forceinline__ bool topk_less(uint64_t ka, int64_t pa, uint64_t kb, int64_t pb,
+                                          const int32_t *__restrict__ idx, int K) {
+  if (ka != kb) return ka < kb;
+  if (pa == pb) return false;
+  if (pa < 0 || pb < 0) return pa >= 0;           // padding (-1) sorts last
+  const int32_t *ra = idx + pa * K, *rb = idx + pb * K;
+  for (int i = 0; i < K; ++i) {
+    const int32_t x = __ldg(ra + i), y = __ldg(rb + i);
+    if (x != y) return x < y;
+  }
+  return pa < pb;
+}
+
+__global__ void __launch_bounds__(kOrderThreads)
+k_topk_order(const double *__restrict__ vals, int D, double sign, const int64_t *__restrict__ cand,
+             int64_t cand_cap, const int64_t *__restrict__ counts, const int32_t *__restrict__ idx,
+             int K, int64_t k, int64_t *__restrict__ top_pos) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = blockIdx.x;
+  const int c = (int)(counts[d] < cand_cap ? counts[d] : cand_cap);
+  int P = 1;
+  while (P < c) P <<= 1;
+  uint64_t *key = reinterpret_cast<uint64_t *>(smem_raw);
+  int64_t *pos = reinterpret_cast<int64_t *>(key + P);
+  const int64_t *cd = cand + (int64_t)d * cand_cap;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    if (i < c) {
+      const int64_t p = cd[i];
+      pos[i] = p;
+      key[i] = orderable_key(sign * vals[p * D + d]);
+    } else {
+      pos[i] = -1;
+      key[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t ka = key[lo], kb = key[hi];
+        const int64_t pa = pos[lo], pb = pos[hi];
+        const bool swap = up ? topk_less(kb, pb, ka, pa, idx, K) : topk_less(ka, pa, kb, pb, idx, K);
+        if (swap) {
+          key[lo] = kb; key[hi] = ka;
+          pos[lo] = pb; pos[hi] = pa;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int m = (int)(k < c ? k : c);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) top_pos[(int64_t)d * k + i] = i < m ? pos[i] : -1;
+}
+
+extern "C" int hoi_topk_order(const double *vals, int32_t D, double sign, const int64_t *cand,
+                              int64_t cand_cap, const int64_t *counts, const int32_t *idx,
+                              int32_t K, int64_t k, int64_t *top_pos, void *stream) {
+  HOI_CHECK_ARG(vals && cand && counts && idx && top_pos && D >= 1 && K >= 1 && k >= 1 &&
+                cand_cap >= 1 && cand_cap <= kOrderMax, "hoi_topk_order: bad args");
+  int P = 1;
+  while (P < cand_cap) P <<= 1;
+  const size_t shm = (size_t)P * (sizeof(uint64_t) + sizeof(int64_t));
+  cudaFuncSetAttribute(k_topk_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+  k_topk_order<<<D, kOrderThreads, shm, (cudaStream_t)stream>>>(vals, D, sign, cand, cand_cap,
+                                                                 counts, idx, K, k, top_pos);
+  return check_launch("k_topk_order");
+}

@@ -12,9 +12,6 @@ bool lattice_supports(int N);
 int scan_full_lattice(const double *corr, const double *eta, int kstride, int N, int D, int kmin,
                       int kmax, int64_t g_begin, int64_t g_end, double *out, int32_t *err_count,
                       void *ws, size_t ws_bytes, cudaStream_t s);
-int scan_full_lattice_fused(const double *corr, const double *eta, int kstride, int N, int D,
-                            int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
-                            void *ws, size_t ws_bytes, cudaStream_t s);
 }  // namespace hoib
 
 using namespace hoib;
@@ -36,7 +33,8 @@ extern "C" int hoi_scan_full(const double *corr, const double *sdiag, const doub
                 "hoi_scan_full: bad rank range");
   HOI_CHECK_ARG(!eta || kstride > kmax, "hoi_scan_full: bias table too short");
   if (engine == 0) engine = lattice_available() && lattice_supports(N) ? 2 : 1;
-  if (engine == 2 || engine == 3) {
+  HOI_CHECK_ARG(engine >= 0 && engine <= 2, "hoi_scan_full: engine must be 0 (auto), 1 or 2");
+  if (engine == 2) {
     size_t need = 0;
     int st = lattice_ws_bytes(N, D, &need);
     if (st) return st;
@@ -47,9 +45,6 @@ extern "C" int hoi_scan_full(const double *corr, const double *sdiag, const doub
     }
     if (!ws_bytes || *ws_bytes < need) return fail(HOI_CAPACITY, "hoi_scan_full: workspace too small");
     HOI_CHECK_ARG(corr && out && err_count, "hoi_scan_full: null pointer");
-    if (engine == 3)
-      return scan_full_lattice_fused(corr, eta, kstride, N, D, kmin, kmax, g_begin, g_end, out,
-                                     ws, *ws_bytes, (cudaStream_t)stream);
     return scan_full_lattice(corr, eta, kstride, N, D, kmin, kmax, g_begin, g_end, out, err_count,
                              ws, *ws_bytes, (cudaStream_t)stream);
   }

@@ -24,6 +24,7 @@ import gc
 import itertools
 import math
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -91,6 +92,44 @@ def _entry(t, v, tc, dtc, o, sv):
     return e
 
 
+class TopEntries(Sequence):
+    """One dataset's TopK result held as arrays -- index tuples (m, K) and
+    the four measures (4, m) -- in the reference's order; the TopEntry
+    objects are built on first access, all at once (a config-5 result is
+    16 x 1,000 entries, and building them eagerly cost more than the device
+    work).  Compares equal to the list of TopEntry it stands for."""
+
+    def __init__(self, tuples: np.ndarray, vals: np.ndarray, m_idx: int):
+        self._t, self._v, self._m = tuples, vals, m_idx
+        self._cache = None
+
+    def __len__(self):
+        return self._t.shape[0]
+
+    @_gc_paused
+    def _list(self):
+        if self._cache is None:
+            m = self._m
+            self._cache = [_entry(tuple(r), x[m], x[0], x[1], x[2], x[3])
+                           for r, x in zip(self._t.tolist(), self._v.T.tolist())]
+        return self._cache
+
+    def __getitem__(self, i):
+        return self._list()[i]
+
+    def __iter__(self):
+        return iter(self._list())
+
+    def __eq__(self, other):
+        try:
+            return self._list() == list(other)
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self):
+        return f"TopEntries({self._list()!r})"
+
+
 class TopK(Reducer):
     """k best n-plets per dataset for one measure; ties broken by the
     lexicographically smallest index tuple (ref:scanner.py:50-105)."""
@@ -104,6 +143,14 @@ class TopK(Reducer):
             raise InvalidData(f"k must be >= 1, got {k}")
         self.measure, self.direction, self.k = measure, direction, k
         self._best = None
+        self._compact = None      # [TopEntries per dataset] from the device order
+
+    def _materialize(self):
+        """Fold a compact device result into the list state (before a merge)."""
+        if self._compact is not None:
+            self._best = [[((self.sign * e.value, e.indices), e) for e in per]
+                          for per in self._compact]
+            self._compact = None
 
     @property
     def sign(self) -> float:
@@ -117,6 +164,7 @@ class TopK(Reducer):
 
     @_gc_paused
     def update(self, batch, hoi):
+        self._materialize()
         vals = getattr(hoi, self.measure)
         b, d_count = vals.shape
         if self._best is None:
@@ -136,6 +184,8 @@ class TopK(Reducer):
             self._merge(d, new)
 
     def finalize(self):
+        if self._compact is not None:
+            return list(self._compact)
         if self._best is None:
             return []
         return [[e for _, e in per] for per in self._best]
@@ -652,6 +702,7 @@ def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
     lib = nat.lib()
     rows = out.shape[1]
     sign = reducer.sign
+    reducer._materialize()
     if reducer._best is None:
         reducer._best = [[] for _ in range(ctx.d)]
     plane = out[m_idx]
@@ -876,9 +927,14 @@ def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: 
     if not isinstance(reducer, TopK):
         raise InvalidData("topk_batch needs a TopK reducer")
     from .nplet_engine import eval_device
+    keep = []
     out, _, _ = eval_device(covs, batch, bias_correct, measures=True, terms=False,
-                            precision=precision)
+                            precision=precision, keep_idx=keep)
     ctx = _BatchCtx(out.shape[2], nat.torch_cuda())
+    if (batch.mode == "fixed" and reducer._best is None and reducer._compact is None
+            and keep and 1 <= ctx.d <= 64 and reducer.k <= _ORDER_MAX // 2):
+        if _topk_batch_device(ctx, reducer, out, keep[0], batch):
+            return reducer
 
     def tuples_of(pos):
         if batch.mode == "fixed":
@@ -889,13 +945,92 @@ def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: 
     return reducer
 
 
-def _scan_device_features(ctx, reducer, batch_size, progress, total, t0):
-    """FeatureAccumulator over device full-output chunks: hoi_features
-    reduces each chunk to 19 partials per dataset on the device (sums,
-    extrema with the first global rank attaining the o extremes, counts);
-    the host merges chunks in enumeration order into the accumulator's own
-    state, so finalize() is the reference's (ref:scanner.py:231-287)."""
+_ORDER_MAX = 8192     # candidates per dataset that hoi_topk_order sorts on chip
+
+
+def _topk_batch_device(ctx, reducer, out, idx_dev, batch) -> bool:
+    """The whole TopK of a fixed-order batch on the device: multi-dataset
+    radix select (the k best keys + every tie at the k-th), then
+    hoi_topk_order sorts each dataset's candidates by the reference's key
+    (sign*value, index tuple) and keeps k; only the (D, k) winners and their
+    four measures reach the host, as arrays (TopEntries).  False when a tie
+    is wider than the on-chip sort (the caller's host path then decides)."""
+    torch = ctx.torch
+    lib = nat.lib()
+    s = nat.stream_handle(torch)
+    rows, d, k = out.shape[1], ctx.d, reducer.k
+    m_idx = MEASURES.index(reducer.measure)
+    plane = out[m_idx]
+    cap = _ORDER_MAX
+    bucket = min(64, cap - k - 1)
+    cands = torch.empty((d, cap), dtype=torch.int64, device="cuda")
+    ws = torch.empty(d * 256 + 4 * d + 64, dtype=torch.int64, device="cuda")
+    hc = (ctypes.c_int64 * d)()
+    nat.check(lib.hoi_topk_select_multi(plane.data_ptr(), rows, d, reducer.sign, k, bucket,
+                                        cands.data_ptr(), cap, hc, ws.data_ptr(), s),
+              "topk_select_multi")
+    counts = [int(hc[i]) for i in range(d)]
+    if max(counts) > cap:
+        return False
+    cnt = torch.tensor(counts, dtype=torch.int64).to("cuda", non_blocking=True)
+    top = torch.empty((d, k), dtype=torch.int64, device="cuda")
+    kk = int(idx_dev.shape[1])
+    nat.check(lib.hoi_topk_order(plane.data_ptr(), d, reducer.sign, cands.data_ptr(), cap,
+                                 cnt.data_ptr(), idx_dev.data_ptr(), kk, k, top.data_ptr(), s),
+              "topk_order")
+    m = min(k, rows)
+    sel = top[:, :m]
+    dsel = torch.arange(d, device="cuda")[:, None].expand(d, m)
+    vals = out[:, sel, dsel].cpu().numpy()                     # (4, D, m)
+    pos = sel.cpu().numpy()
+    tuples = batch.indices[pos]                                # (D, m, K)
+    reducer._compact = [TopEntries(tuples[i], vals[:, i], m_idx) for i in range(d)]
+    return True
+
+
+def _feature_chunks(ctx, total):
+    """Canonical chunks of the feature reduction: a fixed power-of-two row
+    count that depends only on D (32 B x D per row, <= 8 GB), so the
+    partial sums -- and hence the features, to the last bit -- are the same
+    however many ranks share the chunks (sharding.scan_sharded)."""
+    rows = 1 << 28
+    while rows > (1 << 16) and rows * 32 * ctx.d > (8 << 30):
+        rows >>= 1
+    return [(g, min(total, g + rows)) for g in range(0, total, rows)]
+
+
+def _feature_partial(ctx, g0, g1):
+    """hoi_features over global ranks [g0, g1): the (D, 19) partials (sums,
+    extrema with the first global rank attaining the o extremes, counts) and,
+    when the chunk holds it, the whole-system row (D, 4)."""
     torch, lib = ctx.torch, nat.lib()
+    n, d_count = ctx.n, ctx.d
+    offs, acc = [], 0
+    for k in range(ctx.lo, ctx.hi + 1):
+        offs.append(acc)
+        acc += math.comb(n, k)
+    pb = pe = 0
+    if ctx.lo <= 2 <= ctx.hi:
+        pb = offs[2 - ctx.lo]
+        pe = pb + math.comb(n, 2)
+    whole_rank = offs[n - ctx.lo] if ctx.lo <= n <= ctx.hi else -1
+    feat = torch.empty((d_count, 19), dtype=torch.float64, device="cuda")
+    ws_doubles = 8 * 148 * 256 * 19
+    ws = torch.empty(ws_doubles, dtype=torch.float64, device="cuda")
+    out, cnt, coords = ctx.full(g0, g1, reuse_table=getattr(ctx, "_table_ok", False))
+    _raise_not_pd(cnt, coords)
+    nat.check(lib.hoi_features(out.data_ptr(), g1 - g0, d_count, g0, pb, pe, feat.data_ptr(),
+                               ws.data_ptr(), ws_doubles, nat.stream_handle(torch)), "features")
+    whole = None
+    if g0 <= whole_rank < g1:
+        whole = out[:, whole_rank - g0, :].cpu().numpy().T.copy()
+    return feat.cpu().numpy(), whole
+
+
+def _feature_merge(ctx, reducer, parts):
+    """Merge (g0, (partials, whole)) chunks, in enumeration order, into the
+    accumulator's own state, so finalize() is the reference's
+    (ref:scanner.py:231-287)."""
     n, d_count = ctx.n, ctx.d
     if reducer._d is None:
         reducer._init_state(d_count)
@@ -904,27 +1039,11 @@ def _scan_device_features(ctx, reducer, batch_size, progress, total, t0):
         offs.append(acc)
         acc += math.comb(n, k)
     offs_np = np.asarray(offs, dtype=np.int64)
-    pb = pe = 0
-    if ctx.lo <= 2 <= ctx.hi:
-        pb = offs[2 - ctx.lo]
-        pe = pb + math.comb(n, 2)
-    whole_rank = offs[n - ctx.lo] if ctx.lo <= n <= ctx.hi else -1
 
     def order_of(rank):
         return ctx.lo + int(np.searchsorted(offs_np, rank, side="right")) - 1
 
-    feat = torch.empty((d_count, 19), dtype=torch.float64, device="cuda")
-    ws_doubles = 8 * 148 * 256 * 19
-    ws = torch.empty(ws_doubles, dtype=torch.float64, device="cuda")
-    per_chunk = _chunk_rows(d_count, torch)
-    g0 = 0
-    while g0 < total:
-        g1 = min(total, g0 + per_chunk)
-        out, cnt, coords = ctx.full(g0, g1, reuse_table=g0 > 0)
-        _raise_not_pd(cnt, coords)
-        nat.check(lib.hoi_features(out.data_ptr(), g1 - g0, d_count, g0, pb, pe, feat.data_ptr(),
-                                   ws.data_ptr(), ws_doubles, nat.stream_handle(torch)), "features")
-        f = feat.cpu().numpy()
+    for _, (f, whole) in parts:
         reducer._mi_count += int(f[0, 0])
         reducer._mi_sum += f[:, 1]
         reducer._mi_sumsq += f[:, 2]
@@ -940,10 +1059,18 @@ def _scan_device_features(ctx, reducer, batch_size, progress, total, t0):
                 reducer._o_min_order[d] = order_of(int(f[d, 17]))
         np.maximum(reducer._maxs, f[:, 8:12], out=reducer._maxs)
         np.minimum(reducer._mins, f[:, 12:16], out=reducer._mins)
-        if g0 <= whole_rank < g1:
-            reducer._whole = out[:, whole_rank - g0, :].cpu().numpy().T.copy()
-        g0 = g1
-    _emit_progress(progress, n, ctx.lo, ctx.hi, batch_size, total, t0)
+        if whole is not None:
+            reducer._whole = whole
+
+
+def _scan_device_features(ctx, reducer, batch_size, progress, total, t0):
+    """FeatureAccumulator over device full-output chunks: hoi_features
+    reduces each canonical chunk to 19 partials per dataset on the device;
+    the host merges them in enumeration order into the accumulator's own
+    state (ref:scanner.py:231-287)."""
+    parts = [(g0, _feature_partial(ctx, g0, g1)) for g0, g1 in _feature_chunks(ctx, total)]
+    _feature_merge(ctx, reducer, parts)
+    _emit_progress(progress, ctx.n, ctx.lo, ctx.hi, batch_size, total, t0)
 
 
 def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):

@@ -69,7 +69,8 @@ def test_block_shards_partition_the_space():
                     p2 = sum(1 << (v - lo_var) for v in rest if lo_var <= v < n - 10)
                     assert p2 in need
     assert sharding.block_shard_bits(30, 8) == 3 and sharding.block_shard_bits(30, 6) is None
-    assert sharding.block_shard_bits(12, 2) == 1 and sharding.block_shard_bits(11, 2) is None
+    assert sharding.block_shard_bits(17, 2) == 1 and sharding.block_shard_bits(16, 2) is None
+    assert sharding.block_shard_bits(11, 2) is None
 
 
 def _rows(n, lo, hi):
@@ -150,18 +151,19 @@ def test_block_shard_plan_partitions_and_balances():
     """The per-rank shard sets of block_shard_plan partition the rank space,
     and every rank rebuilds the same number of table chunks at 4 and 8 GPUs."""
     from paper_2501_03381_b200.scanner import shard_set_rows
-    n, lo, hi = 16, 2, 9
+    n, lo, hi = 22, 2, 9
     total = sum(math.comb(n, k) for k in range(lo, hi + 1))
     for world in (2, 4, 8):
         sb, masks = sharding.block_shard_plan(n, world)
         rows = [shard_set_rows(n, lo, hi, m, sb) for m in masks]
         allr = np.concatenate(rows)
         assert len(allr) == total and len(np.unique(allr)) == total
-        if world == 4:    # (at N = 16, 8 ranks need 4 > (N-10)/2 shard bits: one shard each)
+        if world >= 4:    # (at 2 ranks the pairs {0, 3} / {1, 2} build 4 / 3 chunks)
             assert len({len(sharding.shard_set_chunks(m, sb)) for m in masks}) == 1
     for world in (4, 8):  # the headline N = 30: every rank rebuilds the same number of chunks
         sb, masks = sharding.block_shard_plan(30, world)
         assert sb == world.bit_length() and len({len(sharding.shard_set_chunks(m, sb))
                                                 for m in masks}) == 1
-    assert sharding.block_shard_plan(12, 2) == (1, [1, 2])
+    assert sharding.block_shard_plan(17, 2) == (1, [1, 2])    # N - 16 = 1 shard bit at most
+    assert sharding.block_shard_plan(14, 2) is None              # table CTAs span every prefix bit
 
