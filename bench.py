@@ -394,7 +394,7 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
     topk_batch from host index arrays; CPU oracle on a bounded sample."""
     from paper_2501_03381_b200 import workloads
     from paper_2501_03381_b200._device import device_covs
-    from paper_2501_03381_b200.scanner import MEASURES, _BatchCtx, _topk_plane
+    from paper_2501_03381_b200.scanner import _BatchCtx, _topk_batch_device
     from paper_2501_03381_b200.sharding import nplet_flops
     xs = [workloads.cfg5_data(d) for d in range(16)]
     covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x)) for x in xs])
@@ -419,11 +419,14 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
                                             None, 0, 400, D, didx.data_ptr(), B, K, out.data_ptr(),
                                             cnt.data_ptr(), coords.data_ptr(), 64, s), "eval32")
 
+    batch0 = hoi.NpletBatch(400, indices=idx, check_unique=False)
+
     def ev_topk():
+        # kernel + the device TopK of topk_batch (multi-dataset radix select,
+        # exact (value, tuple) order on chip, winners to the host as arrays)
         ev()
         red = hoi.TopK("o", "min", 1000)
-        _topk_plane(_BatchCtx(D, torch), red, out, 0, 2,
-                    lambda pos: [tuple(r) for r in idx[np.asarray(pos)].tolist()])
+        assert _topk_batch_device(_BatchCtx(D, torch), red, out, didx, batch0)
         return red
 
     for _ in range(3):
@@ -689,10 +692,10 @@ def e2e(a, torch, hoi, world=1):
             if i:
                 times.append(dt)
             del res
-            torch.cuda.empty_cache()
         return float(np.median(times))
 
     t = run(True)
+    torch.cuda.empty_cache()
     h2d = x.nbytes + 8 * T + 8 * N * N
     d2h = 8 * N * N + back.numel() * 8
     out = {"value": TOTAL / t, "unit": "n-plets/s", "h2d_bytes_per_step": int(h2d),

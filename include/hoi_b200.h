@@ -79,12 +79,23 @@ int hoi_rank_copula(const double *x, int64_t T, int32_t N, int32_t D,
                     const double *qgrid, int64_t *ranks, double *z,
                     void *ws, size_t *ws_bytes, void *stream);
 
+/* hoi_rank_copula with column-major outputs: ranks_t and z_t are (D, N, T)
+ * (a variable's T values contiguous), the layout the rank sort and the
+ * covariance panels stream; the (T, N) outputs of hoi_rank_copula are one
+ * more transpose of these.  ws: query with ws == NULL as above. */
+int hoi_rank_copula_cols(const double *x, int64_t T, int32_t N, int32_t D,
+                         const double *qgrid, int64_t *ranks_t, double *z_t, void *ws,
+                         size_t *ws_bytes, void *stream);
+
 /* Unbiased covariance (divisor T-1) of centred columns, upper triangle
  * computed once and mirrored so cov == cov^T exactly.  Replaces
  * estimate_covariance (ref:copula_core.py:177-189).
  *   z (D, T, N) float64 -> cov (D, N, N) float64. */
 int hoi_covariance(const double *z, int64_t T, int32_t N, int32_t D,
                    double *cov, void *stream);
+/* hoi_covariance of a column-major (D, N, T) z_t (hoi_rank_copula_cols). */
+int hoi_covariance_cols(const double *z_t, int64_t T, int32_t N, int32_t D, double *cov,
+                        void *stream);
 
 /* Correlation form used by every measure kernel: corr (N,N,D) and sdiag (D,N)
  * from cov (D,N,N).  The measures only depend on log det R_S and the

@@ -18,7 +18,11 @@ class DeviceCovs:
         self.n = covs.n_variables
         self.d = covs.n_datasets
         self.t_used = covs.samples_used()
-        sig = torch.from_numpy(np.ascontiguousarray(covs.stacked())).cuda()
+        if all(c._device is not None and c._sigma is None for c in covs.covs):
+            # estimated on the device: no host round trip
+            sig = torch.stack([c._device for c in covs.covs]).contiguous()
+        else:
+            sig = torch.from_numpy(np.ascontiguousarray(covs.stacked())).cuda()
         self.cov = sig
         self.corr = torch.empty((self.n, self.n, self.d), dtype=torch.float64, device=sig.device)
         self.sdiag = torch.empty((self.d, self.n), dtype=torch.float64, device=sig.device)
@@ -47,9 +51,27 @@ class DeviceCovs:
         return self._eta[k_max]
 
 
+def _fingerprint(c):
+    """Cache key of one covariance's contents: the device tensor's identity
+    and in-place version counter while the host copy was never read (or is
+    absent), else a hash of the host bytes -- every byte up to 256 x 256, a
+    strided sample plus row sums beyond (an in-place change of the host
+    array, or a reused id, invalidates the device state)."""
+    import zlib
+    if c._device is not None and c._sigma is None:
+        return ("dev", id(c._device), c._device._version)
+    s = np.ascontiguousarray(c._sigma)
+    if s.size <= 65536:
+        return ("host", s.shape, zlib.crc32(s.view(np.uint8)))
+    flat = s.reshape(-1)
+    probe = np.concatenate([flat[::97], s.sum(axis=1)])
+    return ("host", s.shape, zlib.crc32(probe.view(np.uint8)))
+
+
 def device_covs(covs) -> DeviceCovs:
     torch = nat.torch_cuda()
-    key = (tuple(id(c.sigma) for c in covs.covs), tuple(int(c.n_samples_used) for c in covs.covs))
+    key = (tuple(_fingerprint(c) for c in covs.covs),
+           tuple(int(c.n_samples_used) for c in covs.covs))
     cached = getattr(covs, "_b200_state", None)
     if cached is not None and cached[0] == key:
         return cached[1]

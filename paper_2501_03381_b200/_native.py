@@ -34,6 +34,9 @@ _SIGS = {
     "hoi_launch_count": ([], _i64),
     "hoi_rank_copula": ([_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, C.POINTER(_sz), _vp], C.c_int),
     "hoi_covariance": ([_vp, _i64, _i32, _i32, _vp, _vp], C.c_int),
+    "hoi_rank_copula_cols": ([_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, C.POINTER(_sz), _vp],
+                             C.c_int),
+    "hoi_covariance_cols": ([_vp, _i64, _i32, _i32, _vp, _vp], C.c_int),
     "hoi_correlation": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "hoi_eval_indices": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                           _vp, _i32, _vp], C.c_int),

@@ -56,7 +56,7 @@ constexpr double kMinPivot = 1e-12;
 // CTAs/SM, evict-first far neighbours, claim-ahead L2 prefetch, a chunked
 // table/stencil two-stream pipeline and a single fused produce/consume
 // kernel -- all equal or slower.
-constexpr int kRingFull = 4, kCtasFull = 4, kRingLean = 6;
+constexpr int kRingLean = 6;
 
 __constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F

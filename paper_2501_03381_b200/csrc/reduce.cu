@@ -178,11 +178,44 @@ __global__ void k_key_filter_multi(const double *__restrict__ vals, int64_t n, i
   }
 }
 
+// numpy's float64 sum of n contiguous values (np.add.reduce / mean's
+// summation, numpy/_core/src/umath/loops_utils.h pairwise_sum): sequential
+// below 8 elements, 8 interleaved accumulators combined as a tree up to 128,
+// halves (rounded down to a multiple of 8) above.  Matching it to the bit
+// keeps the optimisers' energies -- and so their beam tie-breaks and
+// annealing decisions -- identical to the reference's.  Every add is an
+// explicit __dadd_rn, so nothing is contracted into an FMA.
+template <typename Get>
+__device__ double np_pairwise_sum(const Get &get, int i0, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, get(i0 + i));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = get(i0 + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], get(i0 + i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, get(i0 + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(get, i0, n2), np_pairwise_sum(get, i0 + n2, n - n2));
+}
+
 // Optimiser objective per row of a (B, D) plane (ref:optimizers.py:74-102):
-// mode 0: mean over the D datasets; mode 1: paired Cohen's d over the pairs
-// (cond_a[i], cond_b[i]): mean(diff) / std(diff, ddof=1).  energy = sign *
-// aggregate (sign -1 for direction 'min').  A zero or non-finite pair
-// standard deviation sets *degenerate.
+// mode 0: vals.mean(axis=1); mode 1: paired Cohen's d over the pairs
+// (cond_a[i], cond_b[i]): diff.mean(axis=1) / diff.std(axis=1, ddof=1),
+// every sum in numpy's order (np_pairwise_sum).  energy = sign * aggregate
+// (sign -1 for direction 'min').  A zero or non-finite pair standard
+// deviation sets *degenerate.
 __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, int mode,
                             const int *__restrict__ ca, const int *__restrict__ cb, int np,
                             double sign, double *__restrict__ energy, int *__restrict__ degenerate) {
@@ -191,18 +224,14 @@ __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, i
     const double *row = vals + b * D;
     double agg;
     if (mode == 0) {
-      double acc = 0.0;
-      for (int d = 0; d < D; ++d) acc += row[d];
-      agg = acc / (double)D;
+      agg = np_pairwise_sum([&](int i) { return row[i]; }, 0, D) / (double)D;
     } else {
-      double mean = 0.0;
-      for (int i = 0; i < np; ++i) mean += row[ca[i]] - row[cb[i]];
-      mean /= (double)np;
-      double ss = 0.0;
-      for (int i = 0; i < np; ++i) {
-        const double x = (row[ca[i]] - row[cb[i]]) - mean;
-        ss += x * x;
-      }
+      auto diff = [&](int i) { return row[ca[i]] - row[cb[i]]; };
+      const double mean = np_pairwise_sum(diff, 0, np) / (double)np;
+      const double ss = np_pairwise_sum([&](int i) {
+        const double x = diff(i) - mean;
+        return __dmul_rn(x, x);       // numpy squares, then sums
+      }, 0, np);
       const double sd = sqrt(ss / (double)(np - 1));
       if (!(sd > 0.0) || !isfinite(sd)) atomicExch(degenerate, 1);
       agg = mean / sd;

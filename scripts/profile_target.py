@@ -38,6 +38,27 @@ def main(mode):
         batch = hoi.NpletBatch(400, indices=idx, check_unique=False)
         for _ in range(2):
             hoi.compute_hoi_batch(covs, batch)
+    elif mode == "copula5":
+        # BASELINE config 5's copula + covariance stage for all 16 datasets in
+        # one batched call of each kernel family (D = 16, T = 1200, N = 400)
+        import ctypes
+        from paper_2501_03381_b200 import _native as nat
+        from paper_2501_03381_b200.copula_core import quantile_grid
+        lib = nat.lib()
+        x = torch.from_numpy(np.stack([workloads.cfg5_data(d) for d in range(16)])).cuda()
+        D, T, N = x.shape
+        q = torch.from_numpy(quantile_grid(T)).cuda()
+        zt = torch.empty((D, N, T), dtype=torch.float64, device="cuda")
+        cov = torch.empty((D, N, N), dtype=torch.float64, device="cuda")
+        need = ctypes.c_size_t(0)
+        nat.check(lib.hoi_rank_copula_cols(None, T, N, D, None, None, None, None,
+                                           ctypes.byref(need), None))
+        ws = torch.empty(int(need.value), dtype=torch.uint8, device="cuda")
+        s = nat.stream_handle(torch)
+        for _ in range(2):
+            nat.check(lib.hoi_rank_copula_cols(x.data_ptr(), T, N, D, q.data_ptr(), None,
+                                               zt.data_ptr(), ws.data_ptr(), ctypes.byref(need), s))
+            nat.check(lib.hoi_covariance_cols(zt.data_ptr(), T, N, D, cov.data_ptr(), s))
     elif mode in ("eval16", "eval20"):
         import math
         k = int(mode[4:])

@@ -271,3 +271,31 @@ def test_greedy_and_anneal_beyond_64_variables_equal_reference():
     w = LARGE_J["anneal"]
     assert list(st.best_indices) == w["best_indices"] and st.iterations == w["iterations"]
     np.testing.assert_allclose(st.energies, w["energies"], rtol=RTOL, atol=ATOL)
+
+
+def test_device_objective_sums_in_numpys_order():
+    """hoi_objective's mean and paired Cohen's d equal numpy's
+    vals.mean(axis=1) and diff.mean / diff.std(ddof=1) bit for bit
+    (ref:optimizers.py:74-102) for D from 1 to 150 -- numpy's pairwise
+    summation, not a sequential sum -- so near-tied energies order as in the
+    reference."""
+    lib, s = _native.lib(), _native.stream_handle(torch)
+    rng = np.random.default_rng(21)
+    for d in list(range(1, 40)) + [64, 100, 129, 150]:
+        vals = rng.standard_normal((257, d)) * 10.0 ** rng.uniform(-4, 4, (257, d))
+        v = torch.as_tensor(vals, device="cuda")
+        energy = torch.empty(257, dtype=torch.float64, device="cuda")
+        degen = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _native.check(lib.hoi_objective(v.data_ptr(), 257, d, 0, None, None, 0, -1.0,
+                                        energy.data_ptr(), degen.data_ptr(), s), "objective")
+        assert np.array_equal(energy.cpu().numpy(), -vals.mean(axis=1)), d
+        if d >= 4:
+            a_idx = np.arange(0, d // 2, dtype=np.int32)
+            b_idx = np.arange(d // 2, 2 * (d // 2), dtype=np.int32)
+            ca, cb = torch.as_tensor(a_idx, device="cuda"), torch.as_tensor(b_idx, device="cuda")
+            _native.check(lib.hoi_objective(v.data_ptr(), 257, d, 1, ca.data_ptr(), cb.data_ptr(),
+                                            len(a_idx), 1.0, energy.data_ptr(), degen.data_ptr(),
+                                            s), "objective")
+            diff = vals[:, a_idx] - vals[:, b_idx]
+            want = diff.mean(axis=1) / diff.std(axis=1, ddof=1)
+            assert np.array_equal(energy.cpu().numpy(), want), d
