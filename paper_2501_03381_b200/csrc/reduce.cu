@@ -210,12 +210,18 @@ __device__ double np_pairwise_sum(const Get &get, int i0, int n) {
   return __dadd_rn(np_pairwise_sum(get, i0, n2), np_pairwise_sum(get, i0 + n2, n - n2));
 }
 
-// Optimiser objective per row of a (B, D) plane (ref:optimizers.py:74-102):
-// mode 0: vals.mean(axis=1); mode 1: paired Cohen's d over the pairs
-// (cond_a[i], cond_b[i]): diff.mean(axis=1) / diff.std(axis=1, ddof=1),
-// every sum in numpy's order (np_pairwise_sum).  energy = sign * aggregate
-// (sign -1 for direction 'min').  A zero or non-finite pair standard
-// deviation sets *degenerate.
+// Optimiser objective per row of a (B, D) plane (ref:optimizers.py:74-102),
+// every sum in the order numpy takes it in the reference:
+//  mode 0: vals.mean(axis=1) -- vals is a C-ordered HoiBatch plane, so the
+//          reduction runs along contiguous rows: np_pairwise_sum;
+//  mode 1: paired Cohen's d over (cond_a[i], cond_b[i]) --
+//          diff = vals[:, cond_a] - vals[:, cond_b] is built by list
+//          indexing, which numpy lays out column-major, so diff.mean(axis=1)
+//          and diff.std(axis=1, ddof=1) reduce along a strided axis with the
+//          row index innermost: plain sequential sums;
+//          energy = mean(diff) / std(diff).
+// energy = sign * aggregate (sign -1 for direction 'min').  A zero or
+// non-finite pair standard deviation sets *degenerate.
 __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, int mode,
                             const int *__restrict__ ca, const int *__restrict__ cb, int np,
                             double sign, double *__restrict__ energy, int *__restrict__ degenerate) {
@@ -226,12 +232,14 @@ __global__ void k_objective(const double *__restrict__ vals, int64_t B, int D, i
     if (mode == 0) {
       agg = np_pairwise_sum([&](int i) { return row[i]; }, 0, D) / (double)D;
     } else {
-      auto diff = [&](int i) { return row[ca[i]] - row[cb[i]]; };
-      const double mean = np_pairwise_sum(diff, 0, np) / (double)np;
-      const double ss = np_pairwise_sum([&](int i) {
-        const double x = diff(i) - mean;
-        return __dmul_rn(x, x);       // numpy squares, then sums
-      }, 0, np);
+      double sum = 0.0;
+      for (int i = 0; i < np; ++i) sum = __dadd_rn(sum, row[ca[i]] - row[cb[i]]);
+      const double mean = sum / (double)np;
+      double ss = 0.0;
+      for (int i = 0; i < np; ++i) {
+        const double x = (row[ca[i]] - row[cb[i]]) - mean;
+        ss = __dadd_rn(ss, __dmul_rn(x, x));      // numpy squares, then sums
+      }
       const double sd = sqrt(ss / (double)(np - 1));
       if (!(sd > 0.0) || !isfinite(sd)) atomicExch(degenerate, 1);
       agg = mean / sd;

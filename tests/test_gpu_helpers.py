@@ -274,11 +274,11 @@ def test_greedy_and_anneal_beyond_64_variables_equal_reference():
 
 
 def test_device_objective_sums_in_numpys_order():
-    """hoi_objective's mean and paired Cohen's d equal numpy's
+    """hoi_objective's mean and paired Cohen's d equal the reference's
     vals.mean(axis=1) and diff.mean / diff.std(ddof=1) bit for bit
-    (ref:optimizers.py:74-102) for D from 1 to 150 -- numpy's pairwise
-    summation, not a sequential sum -- so near-tied energies order as in the
-    reference."""
+    (ref:optimizers.py:74-102) for D from 1 to 150 -- numpy sums the
+    C-ordered plane pairwise and the list-indexed (column-major) diff
+    sequentially -- so near-tied energies order as in the reference."""
     lib, s = _native.lib(), _native.stream_handle(torch)
     rng = np.random.default_rng(21)
     for d in list(range(1, 40)) + [64, 100, 129, 150]:
@@ -296,6 +296,6 @@ def test_device_objective_sums_in_numpys_order():
             _native.check(lib.hoi_objective(v.data_ptr(), 257, d, 1, ca.data_ptr(), cb.data_ptr(),
                                             len(a_idx), 1.0, energy.data_ptr(), degen.data_ptr(),
                                             s), "objective")
-            diff = vals[:, a_idx] - vals[:, b_idx]
+            diff = vals[:, list(a_idx)] - vals[:, list(b_idx)]     # as the reference builds it
             want = diff.mean(axis=1) / diff.std(axis=1, ddof=1)
             assert np.array_equal(energy.cpu().numpy(), want), d
