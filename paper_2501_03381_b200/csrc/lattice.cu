@@ -58,7 +58,9 @@ constexpr double kMinPivot = 1e-12;
 // kernel -- all equal or slower.
 constexpr int kRingLean = 6;
 
-__constant__ double2 c_logtab[256];          // (c_j, L_j) of fast_log
+constexpr int kLogBits = 10;                 // fast_log table index bits
+constexpr int kLogTab = 1 << kLogBits;
+__constant__ double2 c_logtab[kLogTab];      // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
 __constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
 __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
@@ -84,27 +86,39 @@ __device__ __forceinline__ void lp_mul(double &m, int &e, double x) {
 }
 
 // Table-driven FP64 natural log of m * 2^e_extra (m > 0 normal): with
-// x = 2^e * f, f in [1,2), j = top 8 bits of f, c_j = RN(1/(1+j/256)) and
+// x = 2^e * f, f in [1,2), j = top 10 bits of f, c_j = RN(1/(1+j/1024)) and
 // L_j = -log(c_j) (host-evaluated in 80-bit precision), r = f*c_j - 1 lies in
-// [0, 2^-8) and log x = e*ln2 + L_j + log1p(r) with a degree-8 polynomial
-// (truncation < 2^-67).  ~12 FP64 instructions against ~40 for log(); exact
-// 0 for x = 1 (c_0 = 1, L_0 = 0), so identity blocks keep exact zeros.
+// (-2^-52, 2^-10) and log x = e*ln2 + L_j + log1p(r) with a degree-6
+// polynomial (truncation < 2^-72).  ~9 FP64 instructions; exact 0 for
+// x = 1 (c_0 = 1, L_0 = 0), so identity blocks keep exact zeros.  (Round 1
+// used a 256-entry table and degree 8: the 16 KB table costs shared memory
+// the table kernel has spare, and saves two dependent FMAs per log.)
 __device__ __forceinline__ double fast_log(double m, int e_extra, const double2 *__restrict__ tab) {
   const long long b = __double_as_longlong(m);
   const int e = (int)((b >> 52) & 0x7FF) - 1023 + e_extra;
-  const int j = (int)((b >> 44) & 0xFF);
+  const int j = (int)((b >> (52 - kLogBits)) & (kLogTab - 1));
   const double f = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
   const double2 t = tab[j];
   const double r = fma(f, t.x, -1.0);
-  double p = fma(r, -0.125, 0.14285714285714285);
-  p = fma(r, p, -0.16666666666666666);
-  p = fma(r, p, 0.2);
+  double p = fma(r, -0.16666666666666666, 0.2);
   p = fma(r, p, -0.25);
   p = fma(r, p, 0.33333333333333331);
   p = fma(r, p, -0.5);
   p = fma(r, p, 1.0);
   const double ed = (double)e;
   return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(r, p, t.y)));
+}
+
+// 1/x for x > 0 normal: hardware approximation + one cubic Newton step
+// (e = 1 - x r; r' = r (1 + e + e^2)); the ~2^-22 error of the
+// approximation cubes to below double precision (the Schur pivots lie in
+// (1e-12, 1]).  3 DFMA against __drcp_rn's longer correctly rounded
+// sequence with its special-case branch.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // Shared-memory swizzle of a block's 1024 entries: the output pass reads
@@ -135,7 +149,7 @@ struct Leaf {
     // include: pivot a00, Schur complement of the rest
     const double p = a[0];
     bad |= !(p > kMinPivot);
-    const double rp = __drcp_rn(p);
+    const double rp = fast_rcp(p);
     double in[R1 * (R1 + 1) / 2 > 0 ? R1 * (R1 + 1) / 2 : 1];
 #pragma unroll
     for (int i = 1; i < R; ++i) {
@@ -189,7 +203,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   // stacked 2^N doubles apart (scan_full_lattice's multi-dataset batches)
   const int dd = d + (int)blockIdx.y;
   table += (int64_t)blockIdx.y << N;
-  __shared__ double2 s_logtab[256];
+  extern __shared__ double2 s_logtab[];            // kLogTab entries (dynamic: 16 KB)
   constexpr int MS = MAXV + 1;
   constexpr int WS = MAXB + CB;                    // per-warp matrix stride
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
@@ -201,7 +215,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nP = N - CB;
-  for (int x = tid; x < 256; x += NT) s_logtab[x] = c_logtab[x];
+  for (int x = tid; x < kLogTab; x += NT) s_logtab[x] = c_logtab[x];
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
@@ -293,7 +307,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       const bool inc = (lane >> j) & 1;
       const double p = c[j * (j + 1) / 2 + j];
       if (inc && !(p > kMinPivot)) bad = 1;
-      const double f = inc ? __drcp_rn(p) : 0.0;
+      const double f = inc ? fast_rcp(p) : 0.0;
       if (inc) lp_mul(ml, el, p);
 #pragma unroll
       for (int i = j + 1; i < CB; ++i) {
@@ -321,6 +335,22 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   }
   __syncthreads();
   if (tid == 0 && s_bad) atomicExch(flag, 1);
+}
+
+// Table-kernel launch: its fast_log table is 16 KB of dynamic shared memory
+// on top of ~42 KB static (over the 48 KB default).
+template <int NW>
+static void launch_table(dim3 grid, cudaStream_t s, const double *corr, int N, int D, int d, int b,
+                         double *table, int *flag, unsigned cta_off) {
+  constexpr int kDyn = kLogTab * (int)sizeof(double2);
+  static thread_local int set_for = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_for != dev) {
+    cudaFuncSetAttribute(k_lattice_table<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    set_for = dev;
+  }
+  k_lattice_table<NW><<<grid, 32 * NW, kDyn, s>>>(corr, N, D, d, b, table, flag, cta_off);
 }
 
 // TMA bulk-copy / mbarrier helpers (the sm_90+/sm_100 bulk copy engine).
@@ -986,6 +1016,11 @@ struct FullSmem {
   int64_t base[2][CB + 1];
 };
 
+// FAST: one dataset, no bias, the whole rank range, global rows -- the
+// headline configuration -- with every branch of the general epilogue
+// (bias terms, partial-range and local-row checks, the dataset column)
+// resolved at compile time.
+template <bool FAST>
 __global__ void __launch_bounds__(kStencilThreads + 32, 4)
 k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, int kmax,
                const double *__restrict__ eta, int kstride, const int64_t *__restrict__ order_off,
@@ -1145,13 +1180,13 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       const int e = w & 1023, t = (w >> 10) & 1023, q = w >> 20;
       const int64_t b0 = sm.base[buf][q];
       const int k = kP + q;
-      const int64_t row = ps.local ? lrow0 + tid + kStencilThreads * r : b0 + t;
-      const bool valid = b0 != kNoRun && (ps.local || (row >= 0 && row < rows));
+      const int64_t row = (!FAST && ps.local) ? lrow0 + tid + kStencilThreads * r : b0 + t;
+      const bool valid = b0 != kNoRun && (FAST || ps.local || (row >= 0 && row < rows));
       if (!valid) continue;
       const double l = own[swz(e)], nb = sm.nbs[swz(e)];
       const double kd = (double)k;
       double tc, dtc, o;
-      if (et) {
+      if (!FAST && et) {
         const double ek = et[k], ek1 = et[k - 1];
         tc = -0.5 * l - kd * e1 + ek;
         dtc = 0.5 * ((1.0 - kd) * l + nb) + (kd - 1.0) * ek - kd * ek1;
@@ -1163,7 +1198,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       }
       // streaming (evict-first) stores: the 32 B/n-plet output must not
       // push the log-det table's neighbour blocks out of L2
-      const int64_t oi = row * D + dd;
+      const int64_t oi = FAST ? row : row * D + dd;
       __stcs(out + oi, tc);
       __stcs(out + plane + oi, dtc);
       __stcs(out + 2 * plane + oi, o);
@@ -1205,14 +1240,14 @@ void upload_tables() {
     for (int mask : runs[q]) rm[at++] = (uint16_t)mask;
   }
   rs[CB + 1] = (uint16_t)at;
-  std::vector<double2> lt(256);
-  for (int j = 0; j < 256; ++j) {
-    long double c = 1.0L / (1.0L + (long double)j / 256.0L);
+  std::vector<double2> lt(kLogTab);
+  for (int j = 0; j < kLogTab; ++j) {
+    long double c = 1.0L / (1.0L + (long double)j / (long double)kLogTab);
     double cd = (double)c;
     lt[j].x = cd;
     lt[j].y = (double)(-logl((long double)cd));
   }
-  cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * 256);
+  cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * kLogTab);
   cudaMemcpyToSymbol(g_runmask, rm.data(), sizeof(uint16_t) * BLK);
   {
     std::vector<uint32_t> gr(BLK);
@@ -1331,7 +1366,7 @@ int lattice_table(const double *corr, int N, int D, int d, void *ws, size_t ws_b
   if (reset_flag) cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   const int nP = N - CB;
   const int b = nP < MAXB ? nP : MAXB;
-  k_lattice_table<8><<<1u << (nP - b), 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag, 0u);
+  launch_table<8>(dim3(1u << (nP - b)), s, corr, N, D, d, b, w.table, w.flag, 0u);
   return check_launch("k_lattice_table");
 }
 
@@ -1372,32 +1407,46 @@ static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *et
   return check_launch("k_lattice_measures");
 }
 
-static int run_full(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
-                    int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, int64_t plane,
-                    unsigned blk_begin, unsigned blk_end, const uint8_t *active,
-                    const StencilPass &ps, cudaStream_t s) {
+template <bool FAST>
+static int run_full_t(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
+                      int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
+                      int64_t plane, unsigned blk_begin, unsigned blk_end, const uint8_t *active,
+                      const StencilPass &ps, cudaStream_t s) {
   static thread_local int set_for = -1;
   static thread_local int grid_cap = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   const int smem = (int)sizeof(FullSmem);
   if (set_for != dev) {
-    cudaFuncSetAttribute(k_lattice_full, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_lattice_full<FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_full, kStencilThreads + 32,
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lattice_full<FAST>,
+                                                  kStencilThreads + 32, smem);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     set_for = dev;
   }
   const unsigned n = blk_end - blk_begin;
   const unsigned grid = n < (unsigned)grid_cap ? n : (unsigned)grid_cap;
   if (grid == 0) return HOI_OK;
-  k_lattice_full<<<grid, kStencilThreads + 32, smem, s>>>(w.table, N, D, d, kmin, kmax, eta,
-                                                          kstride, w.offs, g_begin, g_end, out,
-                                                          plane, blk_begin, blk_end, active,
-                                                          w.counter, ps);
+  k_lattice_full<FAST><<<grid, kStencilThreads + 32, smem, s>>>(w.table, N, D, d, kmin, kmax, eta,
+                                                                kstride, w.offs, g_begin, g_end,
+                                                                out, plane, blk_begin, blk_end,
+                                                                active, w.counter, ps);
   return check_launch("k_lattice_full");
+}
+
+static int run_full(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
+                    int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out, int64_t plane,
+                    unsigned blk_begin, unsigned blk_end, const uint8_t *active,
+                    const StencilPass &ps, cudaStream_t s) {
+  int64_t h_off[MAXV + 1];
+  const bool whole = g_begin == 0 && g_end == total_rows(N, kmin, kmax, h_off);
+  if (D == 1 && !eta && whole && !ps.local && ps.nstack == 0)
+    return run_full_t<true>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
+                            blk_begin, blk_end, active, ps, s);
+  return run_full_t<false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
+                           blk_begin, blk_end, active, ps, s);
 }
 
 // Persistent stencil launch over table blocks [blk_begin, blk_end): one
@@ -1561,7 +1610,7 @@ int lattice_shard(const double *corr, int N, int D, int d, const double *eta, in
     for (unsigned o = 0; o < (1u << sb) && !need; ++o)
       need = ((mask >> o) & 1ull) && (c & ~o) == 0 && __builtin_popcount(o ^ c) <= 1;
     if (!need) continue;
-    k_lattice_table<8><<<chunk_ctas, 256, 0, s>>>(corr, N, D, d, b, w.table, w.flag,
+    launch_table<8>(dim3(chunk_ctas), s, corr, N, D, d, b, w.table, w.flag,
                                                   c * chunk_ctas);
     if ((st = check_launch("k_lattice_table"))) return st;
   }
@@ -1655,7 +1704,7 @@ int scan_full_lattice(const double *corr, const double *eta, int kstride, int N,
     const int b = nP < MAXB ? nP : MAXB;
     for (int d0 = 0; d0 < D; d0 += slots) {
       const int n = D - d0 < slots ? D - d0 : slots;
-      k_lattice_table<8><<<dim3(1u << (nP - b), (unsigned)n), 256, 0, s>>>(corr, N, D, d0, b,
+      launch_table<8>(dim3(1u << (nP - b), (unsigned)n), s, corr, N, D, d0, b,
                                                                            wb.table, w.flag, 0u);
       int st = check_launch("k_lattice_table");
       if (st) return st;
