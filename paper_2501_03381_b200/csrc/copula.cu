@@ -155,17 +155,22 @@ __global__ void k_rank_merge(int64_t T, int N, int D, int chunk, int nchunks,
   z[out] = qgrid[r];
 }
 
-__global__ void k_col_mean(const double *__restrict__ z, int64_t T, int N, int D,
-                           double *__restrict__ mean) {
-  // one warp per (d, j)
-  int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (w >= D * N) return;
-  const double *zc = z + (int64_t)w * T;       // column-major: contiguous
+// Column means of the column-major (D, N, T) copy: one 256-thread CTA per
+// column, strided partial sums combined in a fixed tree (deterministic).
+__global__ void __launch_bounds__(256) k_col_mean(const double *__restrict__ z, int64_t T,
+                                                  double *__restrict__ mean) {
+  __shared__ double red[8];
+  const double *zc = z + (int64_t)blockIdx.x * T;
   double s = 0.0;
-  for (int64_t t = lane; t < T; t += 32) s += zc[t];
+  for (int64_t t = threadIdx.x; t < T; t += 256) s += zc[t];
+#pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) mean[w] = s / (double)T;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+    mean[blockIdx.x] = a / (double)T;
+  }
 }
 
 // X^T X on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): one 32 x 32
@@ -252,25 +257,35 @@ k_cov(const double *__restrict__ zt, const double *__restrict__ mean, int64_t T,
 }
 
 // Sum of the S slices' partial tiles, slice 0 first (fixed order), scaled
-// by 1/(T-1) and mirrored.
-__global__ void k_cov_reduce(const double *__restrict__ part, int64_t T, int N, int D, int S,
-                             int ntiles, double *__restrict__ cov) {
+// by 1/(T-1) and mirrored: one thread per tile entry, the S slice loads
+// independent (issued together), the adds in slice order.
+__global__ void __launch_bounds__(1024)
+k_cov_reduce(const double *__restrict__ part, int64_t T, int N, int D, int S, int ntiles,
+             double *__restrict__ cov) {
   const int tile = blockIdx.x, d = blockIdx.y;
   const int nt = (N + 31) / 32;
   int ti, tj;
   tile_of(tile, nt, ti, tj);
-  const double inv = 1.0 / (double)(T - 1);
-  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
-    const int li = e >> 5, lj = e & 31;
-    const int i = ti * 32 + li, j = tj * 32 + lj;
-    if (!(i < N && j < N && (ti < tj || i <= j))) continue;
-    double v = 0.0;
-    for (int sl = 0; sl < S; ++sl) v += part[(((int64_t)sl * D + d) * ntiles + tile) * 1024 + e];
-    v *= inv;
-    double *cd = cov + (int64_t)d * N * N;
-    cd[(int64_t)i * N + j] = v;
-    cd[(int64_t)j * N + i] = v;
+  const int e = threadIdx.x;
+  const int li = e >> 5, lj = e & 31;
+  const int i = ti * 32 + li, j = tj * 32 + lj;
+  if (!(i < N && j < N && (ti < tj || i <= j))) return;
+  const double *p = part + ((int64_t)d * ntiles + tile) * 1024 + e;
+  const int64_t step = (int64_t)D * ntiles * 1024;
+  double v = 0.0;
+  int sl = 0;
+  for (; sl + 8 <= S; sl += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(p + (sl + u) * step);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += x[u];
   }
+  for (; sl < S; ++sl) v += __ldg(p + sl * step);
+  v *= 1.0 / (double)(T - 1);
+  double *cd = cov + (int64_t)d * N * N;
+  cd[(int64_t)i * N + j] = v;
+  cd[(int64_t)j * N + i] = v;
 }
 
 __global__ void k_corr(const double *__restrict__ cov, int N, int D,
@@ -301,15 +316,28 @@ __global__ void k_corr(const double *__restrict__ cov, int N, int D,
 using namespace hoib;
 
 namespace {
-// Column-major rank + copula (x already (D, N, T)); ranks_t / z_t (D, N, T).
-int rank_copula_cols(const double *xt, int64_t T, int N, int D, const double *qgrid,
-                     int64_t *ranks_t, double *z_t, char *merge_ws, cudaStream_t s) {
-  int chunk = kMaxChunk;
-  const int nchunks = (int)((T + chunk - 1) / chunk);
-  if (nchunks == 1) {
+// Sort chunk per column: at most kMaxChunk (shared memory), and small
+// enough that the D*N columns give ~2 CTAs per SM (a 2000-sample column of
+// the 30-variable headline system is 8 chunks of 256, not one 2048-wide
+// bitonic network per column on 30 SMs); a column that fits one chunk is
+// ranked directly, otherwise k_rank_merge combines its sorted chunks.
+void pick_chunk(int64_t T, int64_t cols, int &chunk, int &nchunks) {
+  int64_t want = (2 * 148 + cols - 1) / cols;                 // chunks per column
+  int64_t per = (T + want - 1) / want;
+  chunk = 256;
+  while (chunk < per && chunk < kMaxChunk) chunk <<= 1;
+  if (chunk >= T) {                                           // one chunk: pad to 2^k >= T
     chunk = 1;
     while (chunk < T) chunk <<= 1;
   }
+  nchunks = (int)((T + chunk - 1) / chunk);
+}
+
+// Column-major rank + copula (x already (D, N, T)); ranks_t / z_t (D, N, T).
+int rank_copula_cols(const double *xt, int64_t T, int N, int D, const double *qgrid,
+                     int64_t *ranks_t, double *z_t, char *merge_ws, cudaStream_t s) {
+  int chunk, nchunks;
+  pick_chunk(T, (int64_t)N * D, chunk, nchunks);
   const int pad = chunk;
   const size_t shm = (size_t)pad * (sizeof(uint64_t) + sizeof(int));
   cudaFuncSetAttribute(k_rank_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -335,9 +363,10 @@ int rank_copula_cols(const double *xt, int64_t T, int N, int D, const double *qg
 }
 
 size_t merge_bytes(int64_t T, int N, int D) {
-  const int nchunks = (int)((T + kMaxChunk - 1) / kMaxChunk);
+  int chunk, nchunks;
+  pick_chunk(T, (int64_t)N * D, chunk, nchunks);
   if (nchunks == 1) return 0;
-  const size_t elems = (size_t)D * N * nchunks * kMaxChunk;
+  const size_t elems = (size_t)D * N * nchunks * chunk;
   return ((elems * (sizeof(uint64_t) + sizeof(int)) + 255) & ~(size_t)255);
 }
 
@@ -417,7 +446,7 @@ extern "C" int hoi_covariance_cols(const double *z_t, int64_t T, int32_t N, int3
   if (stream_alloc((void **)&mean, sizeof(double) * D * N + pbytes, s) != cudaSuccess)
     return fail(HOI_CUDA_ERROR, "hoi_covariance: cudaMallocAsync failed");
   if (S > 1) part = mean + (size_t)D * N;
-  k_col_mean<<<grid_for((int64_t)D * N * 32, 256), 256, 0, s>>>(z_t, T, N, D, mean);
+  k_col_mean<<<(unsigned)(D * N), 256, 0, s>>>(z_t, T, mean);
   int st = check_launch("k_col_mean");
   if (!st) {
     k_cov<<<dim3((unsigned)ntiles, (unsigned)D, (unsigned)S), 256, 0, s>>>(z_t, mean, T, N, (int)S,
@@ -425,8 +454,8 @@ extern "C" int hoi_covariance_cols(const double *z_t, int64_t T, int32_t N, int3
     st = check_launch("k_cov");
   }
   if (!st && S > 1) {
-    k_cov_reduce<<<dim3((unsigned)ntiles, (unsigned)D), 256, 0, s>>>(part, T, N, D, (int)S,
-                                                                     ntiles, cov);
+    k_cov_reduce<<<dim3((unsigned)ntiles, (unsigned)D), 1024, 0, s>>>(part, T, N, D, (int)S,
+                                                                      ntiles, cov);
     st = check_launch("k_cov_reduce");
   }
   cudaFreeAsync(mean, s);
