@@ -148,3 +148,26 @@ def stream_handle(torch):
 
 def launch_count() -> int:
     return int(lib().hoi_launch_count())
+
+
+def traced(name: str):
+    """Decorator: an NVTX range named `name` around a public entry point, so
+    nsys / ncu timelines show the pipeline's stages (copula, covariance,
+    scan, batch evaluation, TopK, shard) by the reference's names.  The push
+    and pop are host calls of a few hundred nanoseconds; without a CUDA
+    device the call runs unwrapped (its own checks raise as before)."""
+    import functools
+
+    def wrap(fn):
+        @functools.wraps(fn)
+        def run(*args, **kwargs):
+            import torch
+            if not torch.cuda.is_available():
+                return fn(*args, **kwargs)
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return run
+    return wrap

@@ -368,6 +368,7 @@ def eval_device(covs: CovSet, batch: NpletBatch, bias_correct: bool, *, measures
     return out, logdet, invdiag
 
 
+@nat.traced("hoi.entropy_terms")
 def entropy_terms(covs: CovSet, batch: NpletBatch, bias_correct: bool = False) -> EntropyTerms:
     """Joint, marginal and leave-one-out entropies (ref:nplet_engine.py:284-351).
 

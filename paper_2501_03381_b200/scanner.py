@@ -548,6 +548,7 @@ def read_scan(path):
     return head, planes
 
 
+@nat.traced("hoi.scan_device")
 def scan_device(covs: CovSet, min_order: int, max_order: int, *, bias_correct: bool = False,
                 g_begin: int = 0, g_end: int | None = None, engine: int = 0,
                 out=None) -> DeviceScan:
@@ -915,6 +916,7 @@ class _BatchCtx:
         self.d, self.torch = d, torch
 
 
+@nat.traced("hoi.topk_batch")
 def topk_batch(covs: CovSet, batch: NpletBatch, reducer: TopK, *, bias_correct: bool = False,
                precision: str = "fp64"):
     """``reducer.update(batch, compute_hoi_batch(covs, batch, bias_correct))``
@@ -1104,6 +1106,7 @@ def _scan_device_reduce(ctx, reducer, batch_size, progress, total, t0):
     _emit_progress(progress, ctx.n, ctx.lo, ctx.hi, batch_size, total, t0)
 
 
+@nat.traced("hoi.scan")
 def scan(covs: CovSet, min_order: int, max_order: int, reducer: Reducer, *,
          batch_size: int = 10000, bias_correct: bool = False, workers: int = 1, progress=None):
     """Visit every n-plet with order in [min_order, max_order] once
@@ -1140,6 +1143,7 @@ def scan(covs: CovSet, min_order: int, max_order: int, reducer: Reducer, *,
     return reducer.finalize()
 
 
+@nat.traced("hoi.extract_features")
 def extract_features(covs: CovSet, *, bias_correct: bool = False, limit: int = 20,
                      batch_size: int = 10000, workers: int = 1, progress=None):
     """21 features per dataset from one scan of orders 2..N (ref:scanner.py:368-387)."""

@@ -38,6 +38,8 @@ import math
 
 import numpy as np
 
+from . import _native as nat
+
 
 def nplet_flops(k: int) -> float:
     """Algorithmic FP64 flops per (n-plet, dataset) of order k for the
@@ -313,6 +315,7 @@ def _full_local(ctx, plan, rank, fill_nan=False):
     return out, blocks, nblocks
 
 
+@nat.traced("hoi.scan_sharded")
 def scan_sharded(covs, lo, hi, reducer=None, *, bias_correct=False, group=None):
     """This rank's shard of an exhaustive scan on its GPU (one process per
     GPU), merged across the ranks of `group` with the reference's reducer

@@ -1,6 +1,7 @@
 """Small, fixed workloads for ncu captures (one kernel family each).
 
     python scripts/profile_target.py lattice   # cfg4 exhaustive scan, lattice engine
+    python scripts/profile_target.py copula5   # cfg5 copula + covariance (16 x 1200 x 400)
     python scripts/profile_target.py eval10    # cfg5-like batch: K=10, N=400, D=16
     python scripts/profile_target.py eval16    # cfg4 order-16 segment, per-n-plet engine
 """
@@ -20,9 +21,9 @@ from paper_2501_03381_b200.scanner import _ScanCtx  # noqa: E402
 
 def main(mode):
     _build.build()
-    if mode in ("lattice", "fused"):
+    if mode == "lattice":
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
-        ctx = _ScanCtx(covs, 2, 30, False, 2 if mode == "lattice" else 3)
+        ctx = _ScanCtx(covs, 2, 30, False, 2)
         total = hoi.count_nplets(30, 2, 30)
         out = torch.empty((4, total, 1), dtype=torch.float64, device="cuda")
         for _ in range(2):
