@@ -299,3 +299,58 @@ def test_device_objective_sums_in_numpys_order():
             diff = vals[:, list(a_idx)] - vals[:, list(b_idx)]     # as the reference builds it
             want = diff.mean(axis=1) / diff.std(axis=1, ddof=1)
             assert np.array_equal(energy.cpu().numpy(), want), d
+
+
+# ------------------------------------------------- device TopK results --
+
+def test_topk_entries_behave_like_the_reference_lists():
+    """topk_batch's lazy TopEntries: equal to the host reducer's lists,
+    indexable, sliceable, and a later update() merges exactly as the
+    reference's TopK would (the compact state is materialised first)."""
+    rng = np.random.default_rng(8)
+    n = 24
+    a = rng.standard_normal((3 * n, n))
+    sig = a.T @ a / (3 * n) + 0.3 * np.eye(n)
+    covs = hoi.CovSet([hoi.CovarianceMatrix(0.5 * (sig + sig.T)), hoi.CovarianceMatrix(np.eye(n))])
+    idx1 = np.array(sorted({tuple(sorted(rng.choice(n, 6, replace=False))) for _ in range(3000)}))
+    idx2 = np.array(sorted({tuple(sorted(rng.choice(n, 6, replace=False))) for _ in range(3000)}))
+    b1, b2 = hoi.NpletBatch(n, indices=idx1), hoi.NpletBatch(n, indices=idx2)
+    dev = hoi.topk_batch(covs, b1, hoi.TopK("s", "max", 40))
+    got = dev.finalize()
+    host = hoi.TopK("s", "max", 40)
+    host.update(b1, hoi.compute_hoi_batch(covs, b1))
+    want = host.finalize()
+    for g, w in zip(got, want):
+        assert len(g) == len(w) == 40
+        assert g == w and list(g) == w
+        assert g[0] == w[0] and g[-1] == w[-1] and g[3:7] == w[3:7]
+    dev.update(b2, hoi.compute_hoi_batch(covs, b2))
+    host.update(b2, hoi.compute_hoi_batch(covs, b2))
+    assert dev.finalize() == host.finalize()
+    # fewer rows than k: every row, in the reference's order
+    few = hoi.NpletBatch(n, indices=idx1[:5])
+    small = hoi.topk_batch(covs, few, hoi.TopK("o", "min", 10)).finalize()
+    ref = hoi.TopK("o", "min", 10)
+    ref.update(few, hoi.compute_hoi_batch(covs, few))
+    assert small == ref.finalize() and all(len(s) == 5 for s in small)
+
+
+def test_streamed_batch_reports_not_pd_rows_across_chunks():
+    """A 2M-row order-10 batch (streamed to the device in 512k-row chunks)
+    over a covariance whose variables 0 and 1 form an indefinite pair: every
+    row holding both fails the jitter retry, and NotPositiveDefinite names
+    (row, dataset) coordinates of such rows in every chunk they occur."""
+    n = 20
+    sig = np.eye(n)
+    sig[0, 1] = sig[1, 0] = 2.0
+    covs = hoi.CovSet([hoi.CovarianceMatrix(sig)])
+    rng = np.random.default_rng(3)
+    idx = np.sort(np.argsort(rng.random((2_000_000, n)), axis=1)[:, :10], axis=1)
+    bad = np.flatnonzero((idx == 0).any(axis=1) & (idx == 1).any(axis=1))
+    with pytest.raises(hoi.NotPositiveDefinite) as ei:
+        hoi.compute_hoi_batch(covs, hoi.NpletBatch(n, indices=idx, check_unique=False))
+    coords = ei.value.coords
+    assert coords and all(d == 0 for _, d in coords)
+    rows = np.array([r for r, _ in coords])
+    assert np.isin(rows, bad).all()
+    assert len({int(r) // (1 << 19) for r in rows}) >= 2      # coordinates from several chunks

@@ -30,7 +30,7 @@ def _covs(n, seed, d=1):
 CASES = [(18, 2, 18, 1), (18, 3, 9, 2), (14, 2, 14, 1), (10, 2, 10, 1)]   # (N, lo, hi, D)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, tmpdir):
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -49,6 +49,7 @@ def _worker(rank, world, port, q):
             key = f"{n}_{lo}_{hi}_{d}"
             sh = sharding.scan_sharded(covs, lo, hi, None)
             full = sh.gather(0)
+            saved = sh.save(os.path.join(tmpdir, f"{key}.scan"), dst=0)
             top = sharding.scan_sharded(covs, lo, hi, hoi.TopK("o", "min", 25))
             hist = sharding.scan_sharded(covs, lo, hi, hoi.Histogram("tc", 16, 0.0, 2.0))
             feats = None
@@ -59,6 +60,8 @@ def _worker(rank, world, port, q):
                 res[key] = {
                     "kind": sh.kind,
                     "full_equal": bool(torch.equal(full.out, single)),
+                    "save_equal": bool(np.array_equal(hoi.read_scan(saved)[1],
+                                                      single.cpu().numpy())),
                     "local_rows": [sh.local_rows],
                     "top": [[(e.indices, e.o) for e in per] for per in top],
                     "top_single": [[(e.indices, e.o) for e in per]
@@ -88,12 +91,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_ranks_on_one_gpu_equal_the_single_gpu_scan():
+def test_two_ranks_on_one_gpu_equal_the_single_gpu_scan(tmp_path):
     import math
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, str(tmp_path))) for r in range(2)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=600) for _ in procs)
@@ -108,6 +111,7 @@ def test_two_ranks_on_one_gpu_equal_the_single_gpu_scan():
         r0 = got[0][key]
         assert r0["kind"] == ("blocks" if n >= 17 else "ranges")
         assert r0["full_equal"], key
+        assert r0["save_equal"], key            # ShardedScan.save = the single-GPU scan file
         assert r0["top"] == r0["top_single"], key
         assert r0["hist"] == r0["hist_single"], key
         if "feat" in r0:
