@@ -53,6 +53,34 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
+// Table-driven FP64 log (the lattice kernel's fast_log, 256 entries):
+// x = 2^e f, j = top 8 bits of f, r = f c_j - 1 in [0, 2^-8), log x =
+// e ln2 + L_j + log1p(r) with a degree-8 polynomial; ~12 FP64 instructions
+// against ~25 for log().  The table lives in each CTA's shared memory.
+__constant__ double2 c_plog[256];
+
+__device__ __forceinline__ double pipe_log(double m, int e_extra, const double2 *tab) {
+  const long long b = __double_as_longlong(m);
+  const int e = (int)((b >> 52) & 0x7FF) - 1023 + e_extra;
+  const int j = (int)((b >> 44) & 0xFF);
+  const double f = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+  const double2 t = tab[j];
+  const double r = fma(f, t.x, -1.0);
+  double p = fma(r, -0.125, 0.14285714285714285);
+  p = fma(r, p, -0.16666666666666666);
+  p = fma(r, p, 0.2);
+  p = fma(r, p, -0.25);
+  p = fma(r, p, 0.33333333333333331);
+  p = fma(r, p, -0.5);
+  p = fma(r, p, 1.0);
+  const double ed = (double)e;
+  return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(r, p, t.y)));
+}
+
+__device__ __forceinline__ double logprod_value(const LogProd &lp, const double2 *tab) {
+  return pipe_log(lp.m, lp.e, tab);
+}
+
 template <int K>
 __device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &pd) {
   pd.init();
@@ -78,7 +106,7 @@ __device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &
 
 // U = L^-1 in place, then lam = log prod_j (M^-1)_jj, (M^-1)_jj = sum_i U_ij^2 / d_i
 template <int K>
-__device__ __forceinline__ double inv_diag_logprod(double (&a)[K * (K + 1) / 2]) {
+__device__ __forceinline__ LogProd inv_diag_logprod(double (&a)[K * (K + 1) / 2]) {
 #pragma unroll
   for (int j = 0; j < K; ++j) {
 #pragma unroll
@@ -103,7 +131,7 @@ __device__ __forceinline__ double inv_diag_logprod(double (&a)[K * (K + 1) / 2])
     if ((j & 7) == 7) pl.renorm();
   }
   pl.renorm();
-  return pl.log_value();
+  return pl;
 }
 
 constexpr int kPipeThreads = 128;
@@ -113,7 +141,10 @@ __global__ void __launch_bounds__(kPipeThreads, 3) k_eval_pipe(const EvalArgs A)
   constexpr int NE = K * (K - 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *stage = reinterpret_cast<double *>(smem_raw) + threadIdx.x;
+  __shared__ double2 s_plog[256];
   const int tid = threadIdx.x;
+  for (int x = tid; x < 256; x += kPipeThreads) s_plog[x] = c_plog[x];
+  __syncthreads();
   const int D = A.D, N = A.N;
   const int64_t t0 = blockIdx.x * (int64_t)kPipeThreads + tid;
   const int64_t step = (int64_t)gridDim.x * kPipeThreads;   // a multiple of D
@@ -166,8 +197,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3) k_eval_pipe(const EvalArgs A)
       eval_retry<K, true, false>(A, A.src, b, d, K);
       continue;
     }
-    const double lam = inv_diag_logprod<K>(a);
-    finish_unit<K, true, false>(A, b, d, K, s_dummy, true, pd.log_value(), lam, cs_dummy);
+    const LogProd pl = inv_diag_logprod<K>(a);
+    finish_unit<K, true, false>(A, b, d, K, s_dummy, true, logprod_value(pd, s_plog),
+                                logprod_value(pl, s_plog), cs_dummy);
   }
 }
 
@@ -202,12 +234,28 @@ int launch_pipe(const EvalArgs &A, cudaStream_t s) {
 
 // -1 when the launch is not this kernel's (see nplet_eval.cu launch_eval):
 // fixed orders 4..12, FP64 measures only, index rows, R in global memory.
+static void upload_plog() {
+  static thread_local int done_for = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_for == dev) return;
+  double2 t[256];
+  for (int j = 0; j < 256; ++j) {
+    const long double c = 1.0L / (1.0L + (long double)j / 256.0L);
+    t[j].x = (double)c;
+    t[j].y = (double)(-logl((long double)(double)c));
+  }
+  cudaMemcpyToSymbol(c_plog, t, sizeof(t));
+  done_for = dev;
+}
+
 int launch_eval_pipe(const EvalArgs &A, int K, cudaStream_t s) {
   if (A.mats || !A.idx || A.fp32 || A.logdet || A.invdiag || A.row_map || !A.out) return -1;
   if ((size_t)A.N * A.N * A.D * sizeof(double) <= (size_t)kEvalSmemMax) return -1;
   if ((int64_t)A.N * A.N * A.D >= (1ll << 31)) return -1;
   if (A.B * (int64_t)A.D < (int64_t)kPipeThreads * 148) return -1;   // small batches: k_eval
   upload_binomials();
+  upload_plog();
   switch (K) {
     case 4: return launch_pipe<4>(A, s);
     case 5: return launch_pipe<5>(A, s);
