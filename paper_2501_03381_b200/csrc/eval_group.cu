@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
               break;
             }
             pd.mul(dj);
-            const double rp = __drcp_rn(dj);
+            const double rp = pivot_rcp(dj);
             if (t == j % G) dinv[j / G] = rp;
             if (!two) {
 #pragma unroll
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
             }
             pd.mul(dj1);
             if ((j & 7) == 6) pd.renorm();
-            const double rp1 = __drcp_rn(dj1);
+            const double rp1 = pivot_rcp(dj1);
             if (t == (j + 1) % G) dinv[(j + 1) / G] = rp1;
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
             }
             pd.mul(dj);
             if ((j & 7) == 7) pd.renorm();
-            const double rp = __drcp_rn(dj);
+            const double rp = pivot_rcp(dj);
             if (t == j % G) dinv[j / G] = rp;
   #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -334,7 +334,10 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
         sm.red[t][c] = p;
       }
       __syncwarp(gmask);
-      double ls = 0.0;
+      // one log per thread of the product of its columns' (R^-1)_cc (each
+      // >= 1; LogProd keeps the running product in range), not one per column
+      LogProd lp;
+      lp.init();
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const int c = t + G * m;
@@ -342,9 +345,11 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
 #pragma unroll
         for (int q = 0; q < G; ++q) s += sm.red[q][c];
         inv[m] = s;
-        if (c < K) ls += log(s);
+        if (c < K) lp.mul(s);
+        if ((m & 7) == 7) lp.renorm();
       }
-      lam = group_sum<G>(ls, gmask);
+      lp.renorm();
+      lam = group_sum<G>(lp.log_value(), gmask);
       ok = true;
       __syncwarp(gmask);
     }

@@ -21,8 +21,8 @@
 // Arithmetic per unit is k_eval's (ref:nplet_engine.py:267-281 restated as
 // LDL^T + unit-triangular inverse + inverse diagonal, ref:measures.py:41-81
 // epilogue) with two cheaper non-algorithmic pieces: the pivot reciprocal
-// is MUFU.RCP64H refined by one cubic Newton step (3 DFMA; |rel err| <
-// 2^-60, against __drcp_rn's correctly rounded multi-step sequence), and
+// is eval_kernels.cuh's pivot_rcp (MUFU.RCP64H + one quadratic Newton
+// step, shared with k_eval and the group kernel), and
 // the two log products go through k_eval's LogProd.  A non-positive pivot
 // reruns the unit through k_eval's jitter retry (ref:nplet_engine.py:237-264).
 #include "eval_kernels.cuh"
@@ -43,15 +43,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// 1/x for x > 0 normal: hardware approximation + one cubic Newton step
-// (e = 1 - x r; r' = r (1 + e + e^2)); the approximation's ~2^-22 error
-// cubes to below double precision.
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
+
 
 // Table-driven FP64 log (the lattice kernel's fast_log, 256 entries):
 // x = 2^e f, j = top 8 bits of f, r = f c_j - 1 in [0, 2^-8), log x =
@@ -90,7 +82,7 @@ __device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &
     if (!(dj > 0.0)) return false;
     pd.mul(dj);
     if ((j & 7) == 7) pd.renorm();
-    const double r = fast_rcp(dj);
+    const double r = pivot_rcp(dj);
     a[TRI(j, j)] = r;
 #pragma unroll
     for (int i = K - 1; i > j; --i) {
@@ -138,7 +130,6 @@ constexpr int kPipeThreads = 128;
 
 template <int K>
 __global__ void __launch_bounds__(kPipeThreads, 3) k_eval_pipe(const EvalArgs A) {
-  constexpr int NE = K * (K - 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *stage = reinterpret_cast<double *>(smem_raw) + threadIdx.x;
   __shared__ double2 s_plog[256];
