@@ -58,8 +58,9 @@ constexpr double kMinPivot = 1e-12;
 // kernel -- all equal or slower.
 constexpr int kRingLean = 6;
 
-constexpr int kLogBits = 10;                 // fast_log table index bits
+constexpr int kLogBits = 8;                  // fast_log table index bits
 constexpr int kLogTab = 1 << kLogBits;
+constexpr int kLogRep = 8;                   // bank-private replicas in shared memory
 __constant__ double2 c_logtab[kLogTab];      // (c_j, L_j) of fast_log
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
 __constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
@@ -86,21 +87,27 @@ __device__ __forceinline__ void lp_mul(double &m, int &e, double x) {
 }
 
 // Table-driven FP64 natural log of m * 2^e_extra (m > 0 normal): with
-// x = 2^e * f, f in [1,2), j = top 10 bits of f, c_j = RN(1/(1+j/1024)) and
+// x = 2^e * f, f in [1,2), j = top 8 bits of f, c_j = RN(1/(1+j/256)) and
 // L_j = -log(c_j) (host-evaluated in 80-bit precision), r = f*c_j - 1 lies in
-// (-2^-52, 2^-10) and log x = e*ln2 + L_j + log1p(r) with a degree-6
-// polynomial (truncation < 2^-72).  ~9 FP64 instructions; exact 0 for
-// x = 1 (c_0 = 1, L_0 = 0), so identity blocks keep exact zeros.  (Round 1
-// used a 256-entry table and degree 8: the 16 KB table costs shared memory
-// the table kernel has spare, and saves two dependent FMAs per log.)
-__device__ __forceinline__ double fast_log(double m, int e_extra, const double2 *__restrict__ tab) {
+// (-2^-52, 2^-8) and log x = e*ln2 + L_j + log1p(r) with a degree-7
+// polynomial (truncation < 2^-67).  ~10 FP64 instructions; exact 0 for
+// x = 1 (c_0 = 1, L_0 = 0), so identity blocks keep exact zeros.
+// The (c_j, L_j) pairs are random per lane, so one shared table costs ~10
+// wavefronts per warp load (bank conflicts; 81% L1 throughput, the table
+// kernel's top stall in round-2 ncu).  The table is replicated 8 times,
+// entry j of replica q at 16 B x (8 j + q): lane l reads replica l & 7, so
+// the 8 lanes of each quarter-warp phase hit 8 distinct 16-byte bank groups
+// and a warp load is the minimum 4 wavefronts.
+__device__ __forceinline__ double fast_log(double m, int e_extra, const double2 *__restrict__ tab,
+                                           int q) {
   const long long b = __double_as_longlong(m);
   const int e = (int)((b >> 52) & 0x7FF) - 1023 + e_extra;
   const int j = (int)((b >> (52 - kLogBits)) & (kLogTab - 1));
   const double f = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-  const double2 t = tab[j];
+  const double2 t = tab[j * kLogRep + q];
   const double r = fma(f, t.x, -1.0);
-  double p = fma(r, -0.16666666666666666, 0.2);
+  double p = fma(r, 0.14285714285714285, -0.16666666666666666);
+  p = fma(r, p, 0.2);
   p = fma(r, p, -0.25);
   p = fma(r, p, 0.33333333333333331);
   p = fma(r, p, -0.5);
@@ -168,7 +175,7 @@ struct Leaf<0, SW> {
                                              double *__restrict__ out, int lane, int &,
                                              const double2 *__restrict__ tab) {
     // bits holds the F5..F9 pattern at bit positions 5..9
-    out[SW ? swz(bits + lane) : bits + lane] = fast_log(m, e, tab);
+    out[SW ? swz(bits + lane) : bits + lane] = fast_log(m, e, tab, lane & (kLogRep - 1));
   }
 };
 
@@ -182,6 +189,7 @@ __device__ __forceinline__ void schur_lower(double *A, int ld, int n, int j, int
   const int l = j + 1 + (t & 31);
   if (l < n) {
     const double alj = A[l * ld + j] * rp;
+#pragma unroll 4
     for (int i = l + (t >> 5); i < n; i += nt >> 5) A[i * ld + l] = fma(-A[i * ld + j], alj, A[i * ld + l]);
   }
 }
@@ -203,9 +211,12 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   // stacked 2^N doubles apart (scan_full_lattice's multi-dataset batches)
   const int dd = d + (int)blockIdx.y;
   table += (int64_t)blockIdx.y << N;
-  extern __shared__ double2 s_logtab[];            // kLogTab entries (dynamic: 16 KB)
+  extern __shared__ double2 s_logtab[];            // kLogTab x kLogRep entries (dynamic: 32 KB)
   constexpr int MS = MAXV + 1;
-  constexpr int WS = MAXB + CB;                    // per-warp matrix stride
+  // per-warp matrix row stride, odd: schur_lower's lanes read column j of
+  // consecutive rows (A[i][j], i = l..), which at the even stride 16 was a
+  // 16-way bank conflict (87M excess wavefronts in round-2 ncu)
+  constexpr int WS = MAXB + CB + 1;
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
   __shared__ double W[NW][2][WS * WS];             // per-warp base / work (lower triangles)
   __shared__ int vars[MAXV];
@@ -215,7 +226,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nP = N - CB;
-  for (int x = tid; x < kLogTab; x += NT) s_logtab[x] = c_logtab[x];
+  for (int x = tid; x < kLogTab * kLogRep; x += NT) s_logtab[x] = c_logtab[x / kLogRep];
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
@@ -337,12 +348,12 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   if (tid == 0 && s_bad) atomicExch(flag, 1);
 }
 
-// Table-kernel launch: its fast_log table is 16 KB of dynamic shared memory
-// on top of ~42 KB static (over the 48 KB default).
+// Table-kernel launch: its replicated fast_log table is 32 KB of dynamic
+// shared memory on top of ~42 KB static (over the 48 KB default).
 template <int NW>
 static void launch_table(dim3 grid, cudaStream_t s, const double *corr, int N, int D, int d, int b,
                          double *table, int *flag, unsigned cta_off) {
-  constexpr int kDyn = kLogTab * (int)sizeof(double2);
+  constexpr int kDyn = kLogTab * kLogRep * (int)sizeof(double2);
   static thread_local int set_for = -1;
   int dev = 0;
   cudaGetDevice(&dev);

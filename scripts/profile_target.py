@@ -3,7 +3,7 @@
     python scripts/profile_target.py lattice   # cfg4 exhaustive scan, lattice engine
     python scripts/profile_target.py copula5   # cfg5 copula + covariance (16 x 1200 x 400)
     python scripts/profile_target.py eval10    # cfg5-like batch: K=10, N=400, D=16
-    python scripts/profile_target.py eval16    # cfg4 order-16 segment, per-n-plet engine
+    python scripts/profile_target.py eval16    # cfg4 order-16 segment, per-n-plet engine (any order: evalK)
 """
 
 import sys
@@ -60,7 +60,7 @@ def main(mode):
             nat.check(lib.hoi_rank_copula_cols(x.data_ptr(), T, N, D, q.data_ptr(), None,
                                                zt.data_ptr(), ws.data_ptr(), ctypes.byref(need), s))
             nat.check(lib.hoi_covariance_cols(zt.data_ptr(), T, N, D, cov.data_ptr(), s))
-    elif mode in ("eval16", "eval20"):
+    elif mode.startswith("eval") and mode[4:].isdigit():
         import math
         k = int(mode[4:])
         covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(workloads.cfg4()))])
