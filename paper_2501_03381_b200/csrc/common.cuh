@@ -62,13 +62,21 @@ struct LogProd {
   int e;
   __device__ __forceinline__ void init() { m = 1.0; e = 0; }
   __device__ __forceinline__ void mul(double x) { m *= x; }
+  // Fold the exponent into e when |m| leaves [2^-498, 2^499) (frexp's
+  // exact normalisation to [0.5, 1); round 1 used the thresholds 1e-150 and
+  // 1e150 and a branch).  Branch-free: the per-n-plet kernels call it inside
+  // their unrolled factorisations, where a branch splits the straight-line
+  // code the scheduler interleaves.  Denormals are first scaled by 2^54
+  // (exact); zero, inf and NaN pass through unchanged.
   __device__ __forceinline__ void renorm() {
-    double a = fabs(m);
-    if (a < 1e-150 || a > 1e150) {
-      int ex;
-      m = frexp(m, &ex);
-      e += ex;
-    }
+    const int ex0 = (int)((__double_as_longlong(m) >> 52) & 0x7FF);
+    const double ms = ex0 == 0 ? m * 18014398509481984.0 : m;   // 2^54
+    const long long b = __double_as_longlong(ms);
+    const int ex = (int)((b >> 52) & 0x7FF);
+    const bool out = ex != 0 && ex != 0x7FF && (ex < 1023 - 498 || ex > 1023 + 498);
+    const double mn = __longlong_as_double((b & ~(0x7FFll << 52)) | (1022ll << 52));
+    m = out ? mn : m;
+    e += out ? ex - 1022 - (ex0 == 0 ? 54 : 0) : 0;
   }
   __device__ __forceinline__ double log_value() const {
     double l = log(m);

@@ -156,12 +156,16 @@ __device__ __forceinline__ bool ldl_invdiag(TM (&a)[KT * (KT + 1) / 2], int K,
                                             double (&cs)[KT], double &l, double &lam) {
   // the diagonal slot of column j holds 1/d_j once the column is done, so
   // the packed triangle is the only K x K state (fewer live registers)
+  // a non-positive pivot is flagged, not branched on: the factorisation is
+  // one straight-line block the scheduler can overlap across pivots (the
+  // values after a bad pivot are discarded by the caller's retry)
   LogProd pd;
   pd.init();
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const TM dj = a[TRI(j, j)];
-    if (!(dj > TM(0))) return false;
+    bad |= !(dj > TM(0));
     pd.mul((double)dj);
     if ((j & 7) == 7) pd.renorm();
     const TM r = rcp_rn(dj);
@@ -174,6 +178,7 @@ __device__ __forceinline__ bool ldl_invdiag(TM (&a)[KT * (KT + 1) / 2], int K,
       a[TRI(i, j)] = lij;
     }
   }
+  if (bad) return false;
   pd.renorm();
   // U = L^-1 (unit lower), column by column, in place (diagonal untouched).
 #pragma unroll

@@ -76,10 +76,11 @@ __device__ __forceinline__ double logprod_value(const LogProd &lp, const double2
 template <int K>
 __device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &pd) {
   pd.init();
+  bool bad = false;   // flagged, not branched on (see ldl_invdiag)
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double dj = a[TRI(j, j)];
-    if (!(dj > 0.0)) return false;
+    bad |= !(dj > 0.0);
     pd.mul(dj);
     if ((j & 7) == 7) pd.renorm();
     const double r = pivot_rcp(dj);
@@ -93,7 +94,7 @@ __device__ __forceinline__ bool ldl_fast(double (&a)[K * (K + 1) / 2], LogProd &
     }
   }
   pd.renorm();
-  return true;
+  return !bad;
 }
 
 // U = L^-1 in place, then lam = log prod_j (M^-1)_jj, (M^-1)_jj = sum_i U_ij^2 / d_i
