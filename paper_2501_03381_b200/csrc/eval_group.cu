@@ -187,10 +187,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
             }
             __syncwarp(gmask);
             const double dj = v0[j];
-            if (!(dj > 0.0)) {
-              good = false;
-              break;
-            }
+            good &= dj > 0.0;   // flagged, not branched on (see ldl_invdiag)
             pd.mul(dj);
             const double rp = pivot_rcp(dj);
             if (t == j % G) dinv[j / G] = rp;
@@ -215,10 +212,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
             const double u = v0[j + 1];              // a[j+1][j]
             const double l10 = u * rp;               // L[j+1][j]
             const double dj1 = fma(-u, l10, v1[j + 1]);
-            if (!(dj1 > 0.0)) {
-              good = false;
-              break;
-            }
+            good &= dj1 > 0.0;   // flagged, not branched on (see ldl_invdiag)
             pd.mul(dj1);
             if ((j & 7) == 6) pd.renorm();
             const double rp1 = pivot_rcp(dj1);
@@ -253,10 +247,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
               if (G * (m + 1) > j) vec[t + G * m] = a[G * m * (m + 1) / 2 + j];
             __syncwarp(gmask);
             const double dj = vec[j];
-            if (!(dj > 0.0)) {
-              good = false;
-              break;
-            }
+            good &= dj > 0.0;   // flagged, not branched on (see ldl_invdiag)
             pd.mul(dj);
             if ((j & 7) == 7) pd.renorm();
             const double rp = pivot_rcp(dj);
