@@ -47,10 +47,15 @@ struct __align__(16) GrpSmem : GrpCore<G, M> {
   char pad[sizeof(GrpCore<G, M>) % 32 == 16 ? 32 : 16];
 };
 
+// Control flow is warp-uniform (every group of a warp runs the same unit
+// count, attempt count and steps), so group exchanges use full-warp
+// __syncwarp() / shuffles: a partial-mask __syncwarp(gmask) lowers to a
+// MATCH.ANY + REDUX + VOTE convergence check whose latency was ~23% of the
+// (2,9) kernel's stall samples (round-2 ncu, cfg4 order 17).
 template <int G>
-__device__ __forceinline__ double group_sum(double v, unsigned gmask) {
+__device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
@@ -66,7 +71,6 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
   __shared__ __align__(16) GrpSmem<G, M> usm[kGWarps * U];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t = lane % G, g = lane / G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (g * G);
   const int N = A.N, D = A.D;
   const double *src = A.src;
   if (SMEM) {
@@ -77,19 +81,24 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
   }
   GrpSmem<G, M> &sm = usm[w * U + g];
   // each group takes a contiguous chunk of units (dataset fastest): in
-  // unranking mode it unranks once, then steps to the lexicographic successor
+  // unranking mode it unranks once, then steps to the lexicographic successor.
+  // Every group runs `per` iterations; past its chunk's end it recomputes
+  // the last unit and stores nothing (warp-uniform trip count).
   const int64_t units = A.B * (int64_t)D;
   const int64_t ng = (int64_t)gridDim.x * kGWarps * U;
   const int64_t gid = ((int64_t)blockIdx.x * kGWarps + w) * U + g;
   const int64_t per = (units + ng - 1) / ng;
   const int64_t u_begin = gid * per, u_end = u_begin + per < units ? u_begin + per : units;
   int64_t cur_b = -1;
-  for (int64_t u = u_begin; u < u_end; ++u) {
+  for (int64_t it = 0; it < per; ++it) {
+    const bool valid = u_begin + it < u_end;
+    const int64_t u = valid ? u_begin + it : (u_end > u_begin ? u_end - 1 : units - 1);
     const int64_t b = u / D;
     const int d = (int)(u - b * D);
     // ------------------------------------------------------------ indices ----
-    if (b != cur_b) {
-      __syncwarp(gmask);                       // previous unit's idx reads done
+    const bool fresh = b != cur_b;
+    __syncwarp();                              // previous unit's idx reads done
+    if (fresh) {
       if (A.idx) {
 #pragma unroll
         for (int m = 0; m < M; ++m)
@@ -120,8 +129,8 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
         }
       }
       cur_b = b;
-      __syncwarp(gmask);
     }
+    __syncwarp();
     int si[M];
     double sg[M];
 #pragma unroll
@@ -133,7 +142,10 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
     bool ok = false;
     double l = 0.0, lam = 0.0;
     double inv[M];
-    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      // the jitter retry runs for the whole warp when any group needs it;
+      // groups that already have their values recompute and discard
+      if (attempt == 1 && __all_sync(0xffffffffu, ok)) break;
       // ----------------------------------------------------------- gather ----
       double a[S];
 #pragma unroll
@@ -151,7 +163,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
         double tr = 0.0;
 #pragma unroll
         for (int m = 0; m < M; ++m) tr += t + G * m < K ? sg[m] : 0.0;
-        tr = A.sdiag ? group_sum<G>(tr, gmask) : (double)K;
+        tr = A.sdiag ? group_sum<G>(tr) : (double)K;
         const double eps = 1e-10 * tr / (double)K;
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -185,7 +197,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
               if (G * (m + 1) > j) v0[t + G * m] = a[o + j];
               if (G * (m + 1) > j + 1) v1[t + G * m] = a[o + j + 1];
             }
-            __syncwarp(gmask);
+            __syncwarp();
             const double dj = v0[j];
             good &= dj > 0.0;   // flagged, not branched on (see ldl_invdiag)
             pd.mul(dj);
@@ -245,7 +257,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
   #pragma unroll
             for (int m = 0; m < M; ++m)
               if (G * (m + 1) > j) vec[t + G * m] = a[G * m * (m + 1) / 2 + j];
-            __syncwarp(gmask);
+            __syncwarp();
             const double dj = vec[j];
             good &= dj > 0.0;   // flagged, not branched on (see ldl_invdiag)
             pd.mul(dj);
@@ -269,13 +281,9 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
           }
         }
         }
-      if (!good) {
-        __syncwarp(gmask);
-        continue;
-      }
       pd.renorm();
-      l = pd.log_value();
-      __syncwarp(gmask);                       // last LDL step's broadcast reads done
+      const double lt = pd.log_value();
+      __syncwarp();                       // last LDL step's broadcast reads done
       // ------------------------------------------------- W = L^-1 in place ----
 #pragma unroll
       for (int j = 1; j < KT; ++j) {
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
                 vec[c] = a[q];
             }
           }
-          __syncwarp(gmask);
+          __syncwarp();
 #pragma unroll
           for (int m = 0; m < M; ++m) {
             if (G * (m + 1) > j + 1) {
@@ -324,9 +332,10 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
         }
         sm.red[t][c] = p;
       }
-      __syncwarp(gmask);
+      __syncwarp();
       // one log per thread of the product of its columns' (R^-1)_cc (each
       // >= 1; LogProd keeps the running product in range), not one per column
+      const bool take = good && !ok;
       LogProd lp;
       lp.init();
 #pragma unroll
@@ -335,70 +344,81 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
         double s = 0.0;
 #pragma unroll
         for (int q = 0; q < G; ++q) s += sm.red[q][c];
-        inv[m] = s;
+        if (take) inv[m] = s;
         if (c < K) lp.mul(s);
         if ((m & 7) == 7) lp.renorm();
       }
       lp.renorm();
-      lam = group_sum<G>(lp.log_value(), gmask);
-      ok = true;
-      __syncwarp(gmask);
+      const double lamt = group_sum<G>(lp.log_value());
+      if (take) {
+        l = lt;
+        lam = lamt;
+        ok = true;
+      }
+      __syncwarp();
     }
     // ------------------------------------------------------------- output ----
-    const int64_t ob = A.row_map ? A.row_map[b] : A.out_row0 + b;
-    const int64_t o = ob * D + d;
-    if (!ok) {
-      if (t == 0) {
-        const int slot = atomicAdd(A.err_count, 1);
-        if (slot < A.err_cap) {
-          A.err_coords[2 * slot] = ob;
-          A.err_coords[2 * slot + 1] = d;
-        }
-        const double nan = __longlong_as_double(0x7ff8000000000000ll);
-        if (A.out)
-          for (int q = 0; q < 4; ++q) A.out[q * A.plane + o] = nan;
-        if (COMPAT && A.logdet) A.logdet[o] = nan;
-      }
-      continue;
-    }
-    if (A.out && t == 0) {
-      double tc, dtc, oi;
-      const double kd = (double)K;
-      if (A.eta) {
-        const double *e = A.eta + (int64_t)d * A.kstride;
-        const double e1 = e[1], ek = e[K], ek1 = e[K - 1];
-        tc = -0.5 * l - kd * e1 + ek;
-        dtc = 0.5 * (l + lam) + (kd - 1.0) * ek - kd * ek1;
-        oi = -l - 0.5 * lam - kd * e1 - (kd - 2.0) * ek + kd * ek1;
-      } else {
-        tc = -0.5 * l;
-        dtc = 0.5 * (l + lam);
-        oi = -l - 0.5 * lam;
-      }
-      A.out[o] = tc;
-      A.out[A.plane + o] = dtc;
-      A.out[2 * A.plane + o] = oi;
-      A.out[3 * A.plane + o] = tc + dtc;
-    }
+    // (no early exits: the COMPAT group sum below is a full-warp shuffle)
+    double lsg = 0.0;
     if (COMPAT) {
-      // Sigma-space values (entropy_terms compat)
-      double lsg = 0.0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const int c = t + G * m;
-        if (c < K) {
-          if (A.sdiag) lsg += log(sg[m]);
-          if (A.invdiag) {
-            const double v = inv[m] / sg[m];
-            if (A.inv_n > 0)
-              A.invdiag[o * A.inv_n + si[m]] = v;
-            else
-              A.invdiag[o * K + c] = v;
+      for (int m = 0; m < M; ++m)
+        if (t + G * m < K && A.sdiag) lsg += log(sg[m]);
+      lsg = group_sum<G>(lsg);
+    }
+    if (valid) {
+      const int64_t ob = A.row_map ? A.row_map[b] : A.out_row0 + b;
+      const int64_t o = ob * D + d;
+      if (!ok) {
+        if (t == 0) {
+          const int slot = atomicAdd(A.err_count, 1);
+          if (slot < A.err_cap) {
+            A.err_coords[2 * slot] = ob;
+            A.err_coords[2 * slot + 1] = d;
           }
+          const double nan = __longlong_as_double(0x7ff8000000000000ll);
+          if (A.out)
+            for (int q = 0; q < 4; ++q) A.out[q * A.plane + o] = nan;
+          if (COMPAT && A.logdet) A.logdet[o] = nan;
+        }
+      } else {
+        if (A.out && t == 0) {
+          double tc, dtc, oi;
+          const double kd = (double)K;
+          if (A.eta) {
+            const double *e = A.eta + (int64_t)d * A.kstride;
+            const double e1 = e[1], ek = e[K], ek1 = e[K - 1];
+            tc = -0.5 * l - kd * e1 + ek;
+            dtc = 0.5 * (l + lam) + (kd - 1.0) * ek - kd * ek1;
+            oi = -l - 0.5 * lam - kd * e1 - (kd - 2.0) * ek + kd * ek1;
+          } else {
+            tc = -0.5 * l;
+            dtc = 0.5 * (l + lam);
+            oi = -l - 0.5 * lam;
+          }
+          A.out[o] = tc;
+          A.out[A.plane + o] = dtc;
+          A.out[2 * A.plane + o] = oi;
+          A.out[3 * A.plane + o] = tc + dtc;
+        }
+        if (COMPAT) {
+          // Sigma-space values (entropy_terms compat)
+          if (A.invdiag) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              const int c = t + G * m;
+              if (c < K) {
+                const double v = inv[m] / sg[m];
+                if (A.inv_n > 0)
+                  A.invdiag[o * A.inv_n + si[m]] = v;
+                else
+                  A.invdiag[o * K + c] = v;
+              }
+            }
+          }
+          if (A.logdet && t == 0) A.logdet[o] = l + lsg;
         }
       }
-      lsg = group_sum<G>(lsg, gmask);
-      if (A.logdet && t == 0) A.logdet[o] = l + lsg;
     }
   }
 }
