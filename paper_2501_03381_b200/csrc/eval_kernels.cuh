@@ -77,6 +77,23 @@ __device__ __forceinline__ void unrank_lex(uint64_t r, int K, int N, int *s) {
   }
 }
 
+// Lexicographic successor of the K-subset s (s not the last one), register
+// form: every position is a compile-time slot, the rightmost incrementable
+// position p is found with predicates, no runtime-indexed array.
+template <int KT>
+__device__ __forceinline__ void lex_successor(int (&s)[KT], int K, int N) {
+  int p = 0;
+#pragma unroll
+  for (int q = 0; q < KT; ++q)
+    if (q < K && s[q] < N - K + q) p = q;
+  int v = 0;
+#pragma unroll
+  for (int q = 0; q < KT; ++q) {
+    if (q == p) v = s[q] + 1;
+    if (q >= p && q < K) s[q] = v + (q - p);
+  }
+}
+
 // src: the correlation matrix (N, N, D) -- global, or the CTA's shared
 // copy for small N x N x D -- or the raw matrix stack in mats mode.  The
 // correlation form has an exact unit diagonal (k_corr writes 1.0), so only
@@ -302,10 +319,8 @@ __device__ __noinline__ void eval_retry(const EvalArgs &A, const double *src, in
 // path with the reference's jitter rule).
 template <int KT, bool FIXED, bool COMPAT, typename TM = double>
 __device__ __forceinline__ void eval_unit(const EvalArgs &A, const TM *src, int64_t b, int d,
-                                          int kdyn) {
+                                          int kdyn, const int (&s)[KT]) {
   const int K = FIXED ? KT : kdyn;
-  int s[KT];
-  unit_indices<KT, FIXED>(A, b, K, s);
   TM a[KT * (KT + 1) / 2];
   double cs[KT];
   double l = 0.0, lam = 0.0;
@@ -348,11 +363,40 @@ __global__ void __launch_bounds__(128, EvalOcc<KT>::value) k_eval(const EvalArgs
     src = sR;
   }
   const int64_t units = A.B * A.D;
+  const int K = FIXED ? KT : kdyn;
+  int s[KT];
+  if (!A.idx && !A.mats) {
+    // unranking mode (exhaustive segments): each thread takes a contiguous
+    // chunk of units (dataset fastest), unranks its first n-plet once and
+    // steps to the lexicographic successor -- the per-unit unranking was a
+    // serial chain of ~N dependent binomial loads (~20% of k_eval<16>'s
+    // stall samples, round-2 ncu).  Stores are per-thread contiguous.
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t per = (units + nth - 1) / nth;
+    const int64_t u0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * per;
+    const int64_t u1 = u0 + per < units ? u0 + per : units;
+    int64_t cur_b = -1;
+    for (int64_t u = u0; u < u1; ++u) {
+      const int64_t b = u / A.D;
+      const int d = (int)(u - b * A.D);
+      if (b != cur_b) {
+        if (cur_b >= 0) {
+          lex_successor<KT>(s, K, A.N);
+        } else {
+          unrank_lex(A.r0 + (uint64_t)b, K, A.N, s);
+        }
+        cur_b = b;
+      }
+      eval_unit<KT, FIXED, COMPAT, TM>(A, src, b, d, kdyn, s);
+    }
+    return;
+  }
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < units;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = t / A.D;
     const int d = (int)(t - b * A.D);
-    eval_unit<KT, FIXED, COMPAT, TM>(A, src, b, d, kdyn);
+    unit_indices<KT, FIXED>(A, b, K, s);
+    eval_unit<KT, FIXED, COMPAT, TM>(A, src, b, d, kdyn, s);
   }
 }
 
