@@ -391,10 +391,13 @@ def test_mixed_masks_high_orders_vs_oracle(oracle):
     np.testing.assert_allclose(terms.excess_leave_one_out, xl, rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("engine", [2])
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("n,lo,hi", [(12, 1, 12), (13, 2, 13), (16, 3, 9)])
 @pytest.mark.parametrize("bias", [False, True])
 def test_lattice_engine_vs_oracle(oracle, n, lo, hi, bias, engine):
+    """Exhaustive scans through the lattice (2) and the per-n-plet engine in
+    unranking mode (1: per-thread unit chunks stepping the lexicographic
+    successor), whole range and a rank sub-range, vs the oracle."""
     sig = _random_cov(n, n)
     sig = 0.5 * (sig + sig.T)
     covs = hoi.CovSet([hoi.CovarianceMatrix(sig, n_samples_used=500)])
