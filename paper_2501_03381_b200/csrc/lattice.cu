@@ -1390,6 +1390,70 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
   return acc;
 }
 
+// Pass 1 of the two-pass full-output stencil as a column pass: the low-bit
+// neighbour sum S[P] = sum_{j in P_low} T[P ^ 2^j] only couples blocks that
+// share their high prefix bits and only entries at the same position, so a
+// CTA takes one high-bit pattern Ph and a column of kColE adjacent storage
+// positions, stages that column of all 2^LB low-bit blocks in shared memory
+// (2^LB x kColE doubles, one 64-byte segment per block, cp.async), and
+// writes the column of S with every neighbour read from shared memory.
+// Each table entry crosses HBM once and the sums once -- no neighbour block
+// is re-read through L2 (the TMA-ring pass re-read ~5 neighbour blocks per
+// block from L2).  Positions are storage positions, so S keeps T's swizzled
+// layout.  Neighbours are summed in ascending bit order.
+constexpr int kColE = 8;   // entries per column segment (64 B)
+
+template <int LB>
+__global__ void __launch_bounds__(256, 3)
+k_lattice_lowsum(const double *__restrict__ T, double *__restrict__ S, unsigned njobs) {
+  extern __shared__ __align__(16) double sv[];   // [2^LB][kColE]
+  constexpr int NB = 1 << LB;
+  constexpr unsigned kCols = BLK / kColE;
+  const int tid = threadIdx.x;
+  for (unsigned job = blockIdx.x; job < njobs; job += gridDim.x) {
+    const unsigned ph = job / kCols, col = job % kCols;
+    const int64_t base = ((int64_t)ph << LB) * BLK + (int64_t)col * kColE;
+#pragma unroll 4
+    for (int x = tid; x < NB * (kColE / 2); x += 256) {
+      const int pl = x / (kColE / 2), q = x % (kColE / 2);
+      const double *src = T + base + (int64_t)pl * BLK + 2 * q;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sv + pl * kColE + 2 * q)),
+                   "l"(src)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll 2
+    for (int x = tid; x < NB * kColE; x += 256) {
+      const int pl = x / kColE, e = x % kColE;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < LB; ++j)
+        if ((pl >> j) & 1) acc += sv[(pl ^ (1 << j)) * kColE + e];
+      S[base + (int64_t)pl * BLK + e] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+static int launch_lowsum(const double *T, double *S, int nP, int lb, cudaStream_t s) {
+  if (lb != 10) return -1;
+  constexpr int kSmem = (1 << 10) * kColE * (int)sizeof(double);
+  static thread_local int set_for = -1;
+  static thread_local int sms = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_for != dev) {
+    cudaFuncSetAttribute(k_lattice_lowsum<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    set_for = dev;
+  }
+  const unsigned njobs = (1u << (nP - lb)) * (unsigned)(BLK / kColE);
+  const unsigned grid = std::min<unsigned>(njobs, (unsigned)sms * 3u);
+  k_lattice_lowsum<10><<<grid, 256, kSmem, s>>>(T, S, njobs);
+  return check_launch("k_lattice_lowsum");
+}
+
 template <int R, int C, int F, int NB = 2>
 static int run_stencil(const LatticeWs &w, int N, int D, int d, const double *eta, int kstride,
                        int kmin, int kmax, int64_t g_begin, int64_t g_end, double *out,
@@ -1519,11 +1583,16 @@ static int launch_stencil(const LatticeWs &w, int N, int D, int d, const double 
   if (two) {
     // the low pass stores its sums straight from registers: no neighbour-sum
     // buffer or run table, so 6 ring slots fit at 4 CTAs/SM
-    const StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0u, 0};
-    cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
-    int st = run_stencil<kRingLean, 4, MODE_LOWSUM, 0>(w, N, D, d, eta, kstride, kmin, kmax,
-                                                       g_begin, g_end, out, plane, blk_begin,
-                                                       blk_end, active, none, p1, s);
+    // (whole-range scans: the column pass; compacted partial scans keep the
+    // TMA-ring pass over their active blocks)
+    int st = listed ? -1 : launch_lowsum(w.table, w.lowsum, nP, lb, s);
+    if (st < 0) {
+      const StencilPass p1{(1u << lb) - 1u, nullptr, w.lowsum, 0, ps.list, ps.nlist, 0u, 0};
+      cudaMemsetAsync(w.counter, 0, sizeof(unsigned), s);
+      st = run_stencil<kRingLean, 4, MODE_LOWSUM, 0>(w, N, D, d, eta, kstride, kmin, kmax,
+                                                     g_begin, g_end, out, plane, blk_begin,
+                                                     blk_end, active, none, p1, s);
+    }
     if (st) return st;
     ps = StencilPass{all & ~((1u << lb) - 1u), w.lowsum, nullptr, lb, listed ? list2 : nullptr,
                      listed ? cnts + 1 : nullptr, 0u, local_rows ? 1 : 0};
