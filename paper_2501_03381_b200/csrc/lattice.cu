@@ -1393,65 +1393,113 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
 // Pass 1 of the two-pass full-output stencil as a column pass: the low-bit
 // neighbour sum S[P] = sum_{j in P_low} T[P ^ 2^j] only couples blocks that
 // share their high prefix bits and only entries at the same position, so a
-// CTA takes one high-bit pattern Ph and a column of kColE adjacent storage
+// CTA takes one high-bit pattern Ph and a column of E adjacent storage
 // positions, stages that column of all 2^LB low-bit blocks in shared memory
-// (2^LB x kColE doubles, one 64-byte segment per block, cp.async), and
-// writes the column of S with every neighbour read from shared memory.
-// Each table entry crosses HBM once and the sums once -- no neighbour block
-// is re-read through L2 (the TMA-ring pass re-read ~5 neighbour blocks per
-// block from L2).  Positions are storage positions, so S keeps T's swizzled
-// layout.  Neighbours are summed in ascending bit order.
-constexpr int kColE = 8;   // entries per column segment (64 B)
+// (2^LB segments of 8E bytes, cp.async), and writes the column of S with
+// every neighbour read from shared memory.  Each table entry crosses HBM
+// once and each sum once: no neighbour block is re-read through L2 (the
+// TMA-ring pass it replaces re-read ~5 neighbour blocks per block from L2
+// and ran at 4.9 TB/s; this one runs at ~6.2 TB/s, 0.93 of the measured copy
+// rate).  Persistent, one 256-thread CTA per SM, the next column's loads in
+// flight while the current one is summed (two 64-128 KB stages).  Positions
+// are storage positions, so S keeps T's swizzled layout; neighbours are
+// added far bits first, as the TMA-ring pass adds them (compacted partial
+// scans and block shards still run that pass, and their rows must stay
+// bit-identical to the whole-range scan's).  Measured alternatives (cfg4, ncu): one
+// stage of 16-entry columns 3.05 ms, three CTAs/SM of 8-entry columns 3.32,
+// 512 threads 2.90, a loop over the set bits only 4.6 (divergent) -- this
+// form 2.76 ms.
+constexpr int kColThreads = 256;
 
-template <int LB>
-__global__ void __launch_bounds__(256, 3)
-k_lattice_lowsum(const double *__restrict__ T, double *__restrict__ S, unsigned njobs) {
-  extern __shared__ __align__(16) double sv[];   // [2^LB][kColE]
-  constexpr int NB = 1 << LB;
-  constexpr unsigned kCols = BLK / kColE;
-  const int tid = threadIdx.x;
-  for (unsigned job = blockIdx.x; job < njobs; job += gridDim.x) {
-    const unsigned ph = job / kCols, col = job % kCols;
-    const int64_t base = ((int64_t)ph << LB) * BLK + (int64_t)col * kColE;
+template <int LB, int E>
+__device__ __forceinline__ void col_load(const double *__restrict__ T, double *buf, unsigned job) {
+  constexpr int NB = 1 << LB, H = E / 2;
+  constexpr unsigned kCols = BLK / E;
+  const unsigned ph = job / kCols, col = job % kCols;
+  const int64_t base = ((int64_t)ph << LB) * BLK + (int64_t)col * E;
 #pragma unroll 4
-    for (int x = tid; x < NB * (kColE / 2); x += 256) {
-      const int pl = x / (kColE / 2), q = x % (kColE / 2);
-      const double *src = T + base + (int64_t)pl * BLK + 2 * q;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sv + pl * kColE + 2 * q)),
-                   "l"(src)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-    __syncthreads();
+  for (int x = threadIdx.x; x < NB * H; x += kColThreads) {
+    const int pl = x / H, q = x % H;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(buf + pl * E + 2 * q)),
+                 "l"(T + base + (int64_t)pl * BLK + 2 * q)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int LB, int E>
+__device__ __forceinline__ void col_sum(const double *buf, double *__restrict__ S, unsigned job) {
+  constexpr int NB = 1 << LB, H = E / 2;
+  constexpr unsigned kCols = BLK / E;
+  const unsigned ph = job / kCols, col = job % kCols;
+  const int64_t base = ((int64_t)ph << LB) * BLK + (int64_t)col * E;
+  const double2 *b2 = reinterpret_cast<const double2 *>(buf);
 #pragma unroll 2
-    for (int x = tid; x < NB * kColE; x += 256) {
-      const int pl = x / kColE, e = x % kColE;
-      double acc = 0.0;
+  for (int x = threadIdx.x; x < NB * H; x += kColThreads) {
+    const int pl = x / H, q = x % H;
+    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int j = 0; j < LB; ++j)
-        if ((pl >> j) & 1) acc += sv[(pl ^ (1 << j)) * kColE + e];
-      S[base + (int64_t)pl * BLK + e] = acc;
-    }
-    __syncthreads();
+    for (int j = LB - 1; j >= 0; --j)    // far bits first: the TMA-ring pass's order
+      if ((pl >> j) & 1) {
+        const double2 v = b2[(pl ^ (1 << j)) * H + q];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+    *reinterpret_cast<double2 *>(S + base + (int64_t)pl * BLK + 2 * q) = acc;
   }
 }
 
-static int launch_lowsum(const double *T, double *S, int nP, int lb, cudaStream_t s) {
-  if (lb != 10) return -1;
-  constexpr int kSmem = (1 << 10) * kColE * (int)sizeof(double);
-  static thread_local int set_for = -1;
-  static thread_local int sms = 0;
+template <int LB, int E>
+__global__ void __launch_bounds__(kColThreads, 1)
+k_lattice_lowsum(const double *__restrict__ T, double *__restrict__ S, unsigned njobs) {
+  extern __shared__ __align__(16) double sv[];   // [2][2^LB][E]
+  constexpr int STAGE = (1 << LB) * E;
+  unsigned job = blockIdx.x;
+  int cur = 0;
+  if (job < njobs) col_load<LB, E>(T, sv, job);
+  for (; job < njobs; job += gridDim.x) {
+    const unsigned nxt = job + gridDim.x;
+    if (nxt < njobs) {
+      col_load<LB, E>(T, sv + (cur ^ 1) * STAGE, nxt);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    col_sum<LB, E>(sv + cur * STAGE, S, job);
+    __syncthreads();   // the stage is refilled by the next iteration's loads
+    cur ^= 1;
+  }
+}
+
+template <int LB>
+static int launch_lowsum_t(const double *T, double *S, int nP, cudaStream_t s) {
+  constexpr int E = LB >= 11 ? 4 : LB == 10 ? 8 : 16;   // two stages <= 128 KB
+  constexpr int kSmem = 2 * (1 << LB) * E * (int)sizeof(double);
+  static thread_local int set_for = -1, sms = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_for != dev) {
-    cudaFuncSetAttribute(k_lattice_lowsum<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_lattice_lowsum<LB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     set_for = dev;
   }
-  const unsigned njobs = (1u << (nP - lb)) * (unsigned)(BLK / kColE);
-  const unsigned grid = std::min<unsigned>(njobs, (unsigned)sms * 3u);
-  k_lattice_lowsum<10><<<grid, 256, kSmem, s>>>(T, S, njobs);
+  const unsigned njobs = (1u << (nP - LB)) * (unsigned)(BLK / E);
+  const unsigned grid = std::min<unsigned>(njobs, (unsigned)sms);
+  k_lattice_lowsum<LB, E><<<grid, kColThreads, kSmem, s>>>(T, S, njobs);
   return check_launch("k_lattice_lowsum");
+}
+
+// -1: no column kernel for this split (the caller runs the TMA-ring pass)
+static int launch_lowsum(const double *T, double *S, int nP, int lb, cudaStream_t s) {
+  switch (lb) {
+    case 7: return launch_lowsum_t<7>(T, S, nP, s);
+    case 8: return launch_lowsum_t<8>(T, S, nP, s);
+    case 9: return launch_lowsum_t<9>(T, S, nP, s);
+    case 10: return launch_lowsum_t<10>(T, S, nP, s);
+    case 11: return launch_lowsum_t<11>(T, S, nP, s);
+    default: return -1;
+  }
 }
 
 template <int R, int C, int F, int NB = 2>
