@@ -1400,8 +1400,8 @@ static int64_t total_rows(int N, int kmin, int kmax, int64_t *h_off) {
 // once and each sum once: no neighbour block is re-read through L2 (the
 // TMA-ring pass it replaces re-read ~5 neighbour blocks per block from L2
 // and ran at 4.9 TB/s; this one runs at ~6.2 TB/s, 0.93 of the measured copy
-// rate).  Persistent, one 256-thread CTA per SM, the next column's loads in
-// flight while the current one is summed (two 64-128 KB stages).  Positions
+// rate).  Persistent 256-thread CTAs (one per SM at LB = 10), the next
+// column's loads in flight while the current one is summed (two stages).  Positions
 // are storage positions, so S keeps T's swizzled layout; neighbours are
 // added far bits first, as the TMA-ring pass adds them (compacted partial
 // scans and block shards still run that pass, and their rows must stay
@@ -1474,8 +1474,12 @@ k_lattice_lowsum(const double *__restrict__ T, double *__restrict__ S, unsigned 
 
 template <int LB>
 static int launch_lowsum_t(const double *T, double *S, int nP, cudaStream_t s) {
-  constexpr int E = LB >= 11 ? 4 : LB == 10 ? 8 : 16;   // two stages <= 128 KB
+  // two stages <= 128 KB; 16-entry columns measured slower at LB = 9 (3.30
+  // vs 2.74 ms at LB = 10 with 8), and a 9/11 split of cfg4's prefix bits
+  // slower than 10/10 either way (pass 2 +0.5 ms / column pass +1.9 ms)
+  constexpr int E = LB >= 11 ? 4 : 8;
   constexpr int kSmem = 2 * (1 << LB) * E * (int)sizeof(double);
+  constexpr int kPerSm = kSmem <= 64 * 1024 ? 3 : 1;
   static thread_local int set_for = -1, sms = 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1485,7 +1489,7 @@ static int launch_lowsum_t(const double *T, double *S, int nP, cudaStream_t s) {
     set_for = dev;
   }
   const unsigned njobs = (1u << (nP - LB)) * (unsigned)(BLK / E);
-  const unsigned grid = std::min<unsigned>(njobs, (unsigned)sms);
+  const unsigned grid = std::min<unsigned>(njobs, (unsigned)sms * kPerSm);
   k_lattice_lowsum<LB, E><<<grid, kColThreads, kSmem, s>>>(T, S, njobs);
   return check_launch("k_lattice_lowsum");
 }
