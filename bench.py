@@ -395,6 +395,7 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
     from paper_2501_03381_b200 import workloads
     from paper_2501_03381_b200._device import device_covs
     from paper_2501_03381_b200.scanner import _BatchCtx, _topk_batch_device
+    from paper_2501_03381_b200.nplet_engine import index_upload_bytes
     from paper_2501_03381_b200.sharding import nplet_flops
     xs = [workloads.cfg5_data(d) for d in range(16)]
     covs = hoi.CovSet([hoi.estimate_covariance(hoi.copula_transform(x)) for x in xs])
@@ -498,7 +499,7 @@ def cfg5_batched(a, torch, hoi, lib, nat, peak64):
         "fp32_fast_path": {"kernel_ms": kms32, "units_per_s": units / (kms32 * 1e-3),
                            "tolerance": "1e-4 nats absolute vs FP64 (tests/test_gpu_parity.py)"},
         "e2e": {"value": units / e2e_s, "seconds_per_step": e2e_s,
-                "h2d_bytes_per_step": int(idx.size * 4 + sig.nbytes),
+                "h2d_bytes_per_step": int(index_upload_bytes(B, K, 400) + sig.nbytes),
                 "d2h_bytes_per_step": int(len(res) * 1000 * (8 * 5 + 8 * K)),
                 "call": "topk_batch(covs, NpletBatch(400, indices=idx), TopK('o','min',1000))"},
         "roofline": {"bound": "fp64 (gather-limited: 45 f64 of R per unit from L2)",

@@ -244,6 +244,12 @@ def _indices_to_device(indices, torch):
 
 
 _STREAM_ROWS = 1 << 19      # rows per chunk of a streamed index upload
+_INT16_N = 1 << 15          # systems up to this size upload int16 variable ids
+
+
+def index_upload_bytes(b: int, k: int, n: int) -> int:
+    """Host-to-device bytes of a streamed (B, k) index batch over N variables."""
+    return b * k * (2 if n <= _INT16_N else 4)
 _stream_state = {}
 
 
@@ -258,11 +264,17 @@ def _eval_streamed(st, batch, eta, kstride, out, keep_idx):
     b, k = batch.indices.shape
     d, n = st.d, st.n
     dev = torch.cuda.current_device()
+    # variable ids below 2^15 cross PCIe as int16 (half the bytes of the
+    # upload that bounds this path) and are widened to the kernel's int32 on
+    # the copy stream
+    narrow = torch.int16 if n <= _INT16_N else torch.int32
     ss = _stream_state.get(dev)
-    if ss is None or ss["pin"][0].shape[1] != k:
+    if ss is None or ss["pin"][0].shape[1] != k or ss["pin"][0].dtype != narrow:
         ss = {"copy": torch.cuda.Stream(),
-              "pin": [torch.empty((_STREAM_ROWS, k), dtype=torch.int32, pin_memory=True)
-                      for _ in range(2)]}
+              "pin": [torch.empty((_STREAM_ROWS, k), dtype=narrow, pin_memory=True)
+                      for _ in range(2)],
+              "stage": [torch.empty((_STREAM_ROWS, k), dtype=narrow, device="cuda")
+                        for _ in range(2)] if narrow != torch.int32 else None}
         _stream_state[dev] = ss
     src = torch.from_numpy(np.ascontiguousarray(batch.indices))
     idx = torch.empty((b, k), dtype=torch.int32, device="cuda")
@@ -280,7 +292,12 @@ def _eval_streamed(st, batch, eta, kstride, out, keep_idx):
             done[c & 1].synchronize()
         pin[:r1 - r0].copy_(src[r0:r1])
         with torch.cuda.stream(copy):
-            idx[r0:r1].copy_(pin[:r1 - r0], non_blocking=True)
+            if ss["stage"] is None:
+                idx[r0:r1].copy_(pin[:r1 - r0], non_blocking=True)
+            else:
+                stage = ss["stage"][c & 1]
+                stage[:r1 - r0].copy_(pin[:r1 - r0], non_blocking=True)
+                idx[r0:r1].copy_(stage[:r1 - r0])
             ev = torch.cuda.Event()
             ev.record(copy)
         done[c & 1] = ev
