@@ -69,6 +69,7 @@ __global__ void k_topk_filter(const double *__restrict__ vals, int64_t n, int D,
 // resolved key bits equal `prefix` (masked by `hi_mask`).  The digit is
 // masked to `bits`: the last round of a 64-bit select is 4 bits wide at
 // shift 0, and bits 4..11 there are part of the resolved prefix.
+constexpr int kHistUnroll = 8;   // loads in flight per thread in the select / filter passes
 constexpr int kRadixBits = 12;
 constexpr int kRadixBins = 1 << kRadixBits;
 
@@ -82,17 +83,28 @@ k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double si
   __syncthreads();
   int cur = -1;
   unsigned run = 0;     // run-length aggregation (see k_radix_hist_multi)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t key = orderable_key(sign * vals[p * D + d]);
-    if ((key & hi_mask) != prefix) continue;
-    const int b = (int)((key >> shift) & digit_mask);
-    if (b == cur) {
-      ++run;
-    } else {
-      if (run) atomicAdd(&h[cur], run);
-      cur = b;
-      run = 1;
+       p += kHistUnroll * stride) {
+    double v[kHistUnroll];   // independent loads in flight (see k_radix_hist_multi)
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t pp = p + u * stride;
+      v[u] = pp < n ? __ldcs(vals + pp * D + d) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      if (p + u * stride >= n) break;
+      const uint64_t key = orderable_key(sign * v[u]);
+      if ((key & hi_mask) != prefix) continue;
+      const int b = (int)((key >> shift) & digit_mask);
+      if (b == cur) {
+        ++run;
+      } else {
+        if (run) atomicAdd(&h[cur], run);
+        cur = b;
+        run = 1;
+      }
     }
   }
   if (run) atomicAdd(&h[cur], run);
@@ -104,11 +116,23 @@ k_radix_hist(const double *__restrict__ vals, int64_t n, int D, int d, double si
 __global__ void k_key_filter(const double *__restrict__ vals, int64_t n, int D, int d, double sign,
                              uint64_t key_max, int64_t *__restrict__ cand,
                              unsigned long long *__restrict__ count, int64_t cap) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    if (orderable_key(sign * vals[p * D + d]) <= key_max) {
-      unsigned long long slot = atomicAdd(count, 1ull);
-      if ((int64_t)slot < cap) cand[slot] = p;
+       p += kHistUnroll * stride) {
+    double v[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t pp = p + u * stride;
+      v[u] = pp < n ? __ldcs(vals + pp * D + d) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t pp = p + u * stride;
+      if (pp >= n) break;
+      if (orderable_key(sign * v[u]) <= key_max) {
+        unsigned long long slot = atomicAdd(count, 1ull);
+        if ((int64_t)slot < cap) cand[slot] = pp;
+      }
     }
   }
 }
@@ -129,11 +153,13 @@ __global__ void k_radix_hist_multi(const double *__restrict__ vals, int64_t n, i
                                    const int *__restrict__ live, int shift,
                                    unsigned long long *__restrict__ counts) {
   extern __shared__ unsigned int hm[];
-  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+  // one histogram per block (D x 256 counters): with run-length aggregation
+  // the shared atomics are rare (round 1: long runs of one bin; later rounds:
+  // most keys fail the prefix), so per-warp copies only cost occupancy
   const int bins = D * kMBins;
-  for (int i = threadIdx.x; i < nw * bins; i += blockDim.x) hm[i] = 0;
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) hm[i] = 0;
   __syncthreads();
-  unsigned int *my = hm + w * bins;
+  unsigned int *my = hm;
   const int64_t total = n * D;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;     // a multiple of D
@@ -142,24 +168,36 @@ __global__ void k_radix_hist_multi(const double *__restrict__ vals, int64_t n, i
     const uint64_t pre = prefix[d], msk = hi_mask[d];
     int cur = -1;
     unsigned run = 0;
-    for (int64_t t = t0; t < total; t += stride) {
-      const uint64_t key = orderable_key(sign * vals[t]);
-      if ((key & msk) != pre) continue;
-      const int b = (int)((key >> shift) & (kMBins - 1));
-      if (b == cur) {
-        ++run;
-      } else {
-        if (run) atomicAdd(&my[d * kMBins + cur], run);
-        cur = b;
-        run = 1;
+    // kHistUnroll independent loads in flight per thread before any is
+    // binned: one load per iteration left the pass latency-bound (0.77 TB/s
+    // on cfg5's 512 MB, round-2 ncu)
+    for (int64_t t = t0; t < total; t += kHistUnroll * stride) {
+      double v[kHistUnroll];
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) {
+        const int64_t tt = t + u * stride;
+        v[u] = tt < total ? __ldcs(vals + tt) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) {
+        if (t + u * stride >= total) break;
+        const uint64_t key = orderable_key(sign * v[u]);
+        if ((key & msk) != pre) continue;
+        const int b = (int)((key >> shift) & (kMBins - 1));
+        if (b == cur) {
+          ++run;
+        } else {
+          if (run) atomicAdd(&my[d * kMBins + cur], run);
+          cur = b;
+          run = 1;
+        }
       }
     }
     if (run) atomicAdd(&my[d * kMBins + cur], run);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < bins; i += blockDim.x) {
-    unsigned v = 0;
-    for (int x = 0; x < nw; ++x) v += hm[x * bins + i];
+    const unsigned v = hm[i];
     if (v) atomicAdd(&counts[i], (unsigned long long)v);
   }
 }
@@ -167,13 +205,29 @@ __global__ void k_radix_hist_multi(const double *__restrict__ vals, int64_t n, i
 __global__ void k_key_filter_multi(const double *__restrict__ vals, int64_t n, int D, double sign,
                                    const uint64_t *__restrict__ key_max, int64_t *__restrict__ cand,
                                    unsigned long long *__restrict__ count, int64_t cap) {
+  // blockDim.x is a multiple of D (see the launch): every thread keeps one
+  // dataset, and its row advances by stride / D per step (no 64-bit division)
   const int64_t total = n * D;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int d = (int)(t % D);
-    if (orderable_key(sign * vals[t]) <= key_max[d]) {
-      const unsigned long long slot = atomicAdd(&count[d], 1ull);
-      if ((int64_t)slot < cap) cand[(int64_t)d * cap + slot] = t / D;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int d = (int)(t0 % D);
+  const uint64_t km = key_max[d];
+  const int64_t rstep = stride / D;
+  int64_t row = t0 / D;
+  for (int64_t t = t0; t < total; t += kHistUnroll * stride, row += kHistUnroll * rstep) {
+    double v[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t tt = t + u * stride;
+      v[u] = tt < total ? __ldcs(vals + tt) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      if (t + u * stride >= total) break;
+      if (orderable_key(sign * v[u]) <= km) {
+        const unsigned long long slot = atomicAdd(&count[d], 1ull);
+        if ((int64_t)slot < cap) cand[(int64_t)d * cap + slot] = row + u * rstep;
+      }
     }
   }
 }
@@ -462,13 +516,10 @@ extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, d
   std::vector<uint64_t> prefix(D, 0), mask(D, 0), keymax(D, ~0ull);
   std::vector<int64_t> need(D, k < n ? k : n);
   std::vector<int> live(D, k < n ? 1 : 0);
-  // warps per block: D x 256 x 4 B of private histogram per warp, <= 64 KB
-  int nw = (64 * 1024) / (D * kMBins * 4);
-  nw = nw < 1 ? 1 : (nw > 8 ? 8 : nw);
-  int bs = 32 * nw;
-  bs = (bs / D) * D;                              // a multiple of D: one dataset per thread
-  if (bs < D) bs = D;
-  const size_t shm = sizeof(unsigned int) * D * kMBins * ((bs + 31) / 32);
+  // 256-thread blocks (a multiple of D: one dataset per thread), one
+  // D x 256 histogram each (16 KB at D = 16: 8 blocks, 64 warps per SM)
+  const int bs = (256 / D) * D;
+  const size_t shm = sizeof(unsigned int) * D * kMBins;
   const int blocks = 8 * sm_count();
   cudaFuncSetAttribute(k_radix_hist_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
   for (int shift = 64 - kMBits; shift >= 0; shift -= kMBits) {
@@ -505,8 +556,8 @@ extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, d
   unsigned long long *ccount = reinterpret_cast<unsigned long long *>(d_live + 64);
   cudaMemcpyAsync(d_keymax, keymax.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(ccount, 0, sizeof(unsigned long long) * D, s);
-  k_key_filter_multi<<<8 * sm_count(), 256, 0, s>>>(vals, n, D, sign, d_keymax, cand, ccount,
-                                                     cand_cap);
+  k_key_filter_multi<<<8 * sm_count(), bs, 0, s>>>(vals, n, D, sign, d_keymax, cand, ccount,
+                                                    cand_cap);
   int st = check_launch("k_key_filter_multi");
   if (st) return st;
   std::vector<unsigned long long> c(D);
