@@ -336,8 +336,9 @@ def eval_device(covs: CovSet, batch: NpletBatch, bias_correct: bool, *, measures
     torch = st.torch
     lib = nat.lib()
     b, d, n = batch.batch_size, st.d, st.n
-    orders = batch.orders()
-    eta = st.eta(int(orders.max())) if bias_correct else None
+    eta = None
+    if bias_correct:   # (a fixed-order batch's order without materialising (B,) orders)
+        eta = st.eta(batch.order if batch.mode == "fixed" else int(batch.orders().max()))
     kstride = 0 if eta is None else eta.shape[1]
     out = torch.empty((4, b, d), dtype=torch.float64, device="cuda") if measures else None
     cnt, coords = _err_buffers(torch)
