@@ -308,7 +308,8 @@ int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t d, double 
  * hoi_topk_select for all D datasets of a (n, D) plane at once (D <= 64;
  * 8-bit radix digits, per-dataset histograms): dataset d's candidate
  * positions go to cand[d * cand_cap ...] and their count to h_counts[d]
- * (HOST array of D).  ws: device workspace of >= D*256 + 4*D + 64 uint64. */
+ * (HOST array of D).  ws: device workspace of >= D*256 + 5*D + 32 uint64.
+ * The radix rounds run without host round trips; one sync at the end. */
 int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign, int64_t k,
                           int64_t bucket_cap, int64_t *cand, int64_t cand_cap,
                           int64_t *h_counts, void *ws, void *stream);

@@ -500,6 +500,32 @@ extern "C" int hoi_topk_select(const double *vals, int64_t n, int32_t D, int32_t
 // candidates of dataset d go to cand[d * cand_cap ...], their count to
 // h_counts[d] (HOST).  ws: device workspace of at least
 // D * 256 + 4 * D + 64 uint64.  Synchronous.
+// One radix round's bookkeeping for every live dataset, on the device (the
+// host used to read the histograms back after every round: three syncs and
+// round trips per cfg5 TopK): find the bucket holding the need-th key,
+// narrow the prefix, and retire the dataset once that bucket holds at most
+// bucket_cap keys (or the last digit is resolved).
+__global__ void k_radix_step_multi(const unsigned long long *__restrict__ counts, int D, int shift,
+                                   int64_t bucket_cap, uint64_t *prefix, uint64_t *mask,
+                                   uint64_t *keymax, int64_t *need, int *live) {
+  const int d = threadIdx.x;
+  if (d >= D || !live[d]) return;
+  const unsigned long long *hd = counts + (size_t)d * kMBins;
+  const int64_t nd = need[d];
+  int64_t acc = 0;
+  int b = 0;
+  for (; b < kMBins - 1; ++b) {
+    if (acc + (int64_t)hd[b] >= nd) break;
+    acc += (int64_t)hd[b];
+  }
+  need[d] = nd - acc;
+  const uint64_t pre = prefix[d] | ((uint64_t)b << shift);
+  prefix[d] = pre;
+  mask[d] |= (uint64_t)(kMBins - 1) << shift;
+  keymax[d] = pre | (shift ? ((1ull << shift) - 1) : 0ull);
+  if ((int64_t)hd[b] <= bucket_cap || shift == 0) live[d] = 0;
+}
+
 extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, double sign,
                                      int64_t k, int64_t bucket_cap, int64_t *cand,
                                      int64_t cand_cap, int64_t *h_counts, void *ws,
@@ -507,54 +533,46 @@ extern "C" int hoi_topk_select_multi(const double *vals, int64_t n, int32_t D, d
   HOI_CHECK_ARG(vals && cand && h_counts && ws && D >= 1 && D <= 64 && k >= 1 && n >= 0,
                 "hoi_topk_select_multi: bad args");
   cudaStream_t s = (cudaStream_t)stream;
+  // ws: counts (D x 256) | prefix | mask | keymax | need (D each) | live
+  // (64 int) | candidate counts (D)
   unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
   uint64_t *d_prefix = reinterpret_cast<uint64_t *>(counts + (size_t)D * kMBins);
   uint64_t *d_mask = d_prefix + D;
   uint64_t *d_keymax = d_mask + D;
-  int *d_live = reinterpret_cast<int *>(d_keymax + D);
-  std::vector<unsigned long long> h((size_t)D * kMBins);
-  std::vector<uint64_t> prefix(D, 0), mask(D, 0), keymax(D, ~0ull);
-  std::vector<int64_t> need(D, k < n ? k : n);
-  std::vector<int> live(D, k < n ? 1 : 0);
+  int64_t *d_need = reinterpret_cast<int64_t *>(d_keymax + D);
+  int *d_live = reinterpret_cast<int *>(d_need + D);
+  unsigned long long *ccount = reinterpret_cast<unsigned long long *>(d_live + 64);
+  {
+    std::vector<uint64_t> init((size_t)4 * D);
+    for (int d = 0; d < D; ++d) {
+      init[d] = 0;                                  // prefix
+      init[D + d] = 0;                              // mask
+      init[2 * D + d] = ~0ull;                      // keymax
+      init[3 * D + d] = (uint64_t)(k < n ? k : n);  // need
+    }
+    std::vector<int> live(64, 0);
+    for (int d = 0; d < D; ++d) live[d] = k < n ? 1 : 0;
+    cudaMemcpyAsync(d_prefix, init.data(), sizeof(uint64_t) * 4 * D, cudaMemcpyHostToDevice, s);
+    // (pageable sources: staged before the calls return, so the vectors may
+    // go out of scope)
+    cudaMemcpyAsync(d_live, live.data(), sizeof(int) * 64, cudaMemcpyHostToDevice, s);
+  }
   // 256-thread blocks (a multiple of D: one dataset per thread), one
-  // D x 256 histogram each (16 KB at D = 16: 8 blocks, 64 warps per SM)
+  // D x 256 histogram each (16 KB at D = 16: 8 blocks, 64 warps per SM);
+  // every round is launched, a retired dataset's threads skip their loads
   const int bs = (256 / D) * D;
   const size_t shm = sizeof(unsigned int) * D * kMBins;
   const int blocks = 8 * sm_count();
   cudaFuncSetAttribute(k_radix_hist_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
   for (int shift = 64 - kMBits; shift >= 0; shift -= kMBits) {
-    bool any = false;
-    for (int d = 0; d < D; ++d) any = any || live[d];
-    if (!any) break;
     cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * D * kMBins, s);
-    cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(d_mask, mask.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(d_live, live.data(), sizeof(int) * D, cudaMemcpyHostToDevice, s);
     k_radix_hist_multi<<<blocks, bs, shm, s>>>(vals, n, D, sign, d_prefix, d_mask, d_live, shift,
                                                counts);
-    int st = check_launch("k_radix_hist_multi");
+    k_radix_step_multi<<<1, 64, 0, s>>>(counts, D, shift, bucket_cap, d_prefix, d_mask, d_keymax,
+                                        d_need, d_live);
+    int st = check_launch("k_radix_hist_multi/k_radix_step_multi");
     if (st) return st;
-    cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * D * kMBins,
-                    cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    for (int d = 0; d < D; ++d) {
-      if (!live[d]) continue;
-      int64_t acc = 0;
-      int b = 0;
-      const unsigned long long *hd = h.data() + (size_t)d * kMBins;
-      for (; b < kMBins; ++b) {
-        if (acc + (int64_t)hd[b] >= need[d]) break;
-        acc += (int64_t)hd[b];
-      }
-      need[d] -= acc;
-      prefix[d] |= (uint64_t)b << shift;
-      mask[d] |= (uint64_t)(kMBins - 1) << shift;
-      keymax[d] = prefix[d] | (shift ? ((1ull << shift) - 1) : 0ull);
-      if ((int64_t)hd[b] <= bucket_cap || shift == 0) live[d] = 0;
-    }
   }
-  unsigned long long *ccount = reinterpret_cast<unsigned long long *>(d_live + 64);
-  cudaMemcpyAsync(d_keymax, keymax.data(), sizeof(uint64_t) * D, cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(ccount, 0, sizeof(unsigned long long) * D, s);
   k_key_filter_multi<<<8 * sm_count(), bs, 0, s>>>(vals, n, D, sign, d_keymax, cand, ccount,
                                                     cand_cap);

@@ -715,7 +715,7 @@ def _topk_plane(ctx, reducer, out, g0, m_idx, tuples_of=None):
     if ctx.d > 1:
         # every dataset of the plane in one multi-dataset radix select
         cands = torch.empty((ctx.d, cap), dtype=torch.int64, device="cuda")
-        ws = torch.empty(ctx.d * 256 + 4 * ctx.d + 64, dtype=torch.int64, device="cuda")
+        ws = torch.empty(ctx.d * 256 + 5 * ctx.d + 32, dtype=torch.int64, device="cuda")
         hc = (ctypes.c_int64 * ctx.d)()
         nat.check(lib.hoi_topk_select_multi(plane.data_ptr(), rows, ctx.d, sign, reducer.k,
                                             bucket_cap, cands.data_ptr(), cap, hc,
@@ -966,7 +966,7 @@ def _topk_batch_device(ctx, reducer, out, idx_dev, batch) -> bool:
     cap = _ORDER_MAX
     bucket = min(64, cap - k - 1)
     cands = torch.empty((d, cap), dtype=torch.int64, device="cuda")
-    ws = torch.empty(d * 256 + 4 * d + 64, dtype=torch.int64, device="cuda")
+    ws = torch.empty(d * 256 + 5 * d + 32, dtype=torch.int64, device="cuda")
     hc = (ctypes.c_int64 * d)()
     nat.check(lib.hoi_topk_select_multi(plane.data_ptr(), rows, d, reducer.sign, k, bucket,
                                         cands.data_ptr(), cap, hc, ws.data_ptr(), s),
