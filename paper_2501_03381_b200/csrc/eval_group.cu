@@ -67,8 +67,11 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
   // 3.2-3.7 -> 4.4-5.2 TF/s, (4,5) K 19-20 +4%; (4,6) and (4,7) run 2-5%
   // slower blocked (more spills), so they keep one column per broadcast.
   constexpr bool kBlocked2 = G == 2 || (G == 4 && M == 5);
-  extern __shared__ __align__(16) double dynR[];
-  __shared__ __align__(16) GrpSmem<G, M> usm[kGWarps * U];
+  // dynamic shared memory: the groups' exchange slots (sizes above the 48 KB
+  // static limit for (2,10)), then the CTA's copy of R in SMEM mode
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  GrpSmem<G, M> *usm = reinterpret_cast<GrpSmem<G, M> *>(dyn_raw);
+  double *dynR = reinterpret_cast<double *>(dyn_raw + sizeof(GrpSmem<G, M>) * kGWarps * U);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t = lane % G, g = lane / G;
   const int N = A.N, D = A.D;
@@ -426,15 +429,17 @@ __global__ void __launch_bounds__(32 * kGWarps, MINB) k_eval_grp(const EvalArgs 
 template <int G, int M, int MINB, bool COMPAT, bool SMEM>
 int launch_grp(const EvalArgs &A, int K, cudaStream_t s) {
   auto kern = k_eval_grp<G, M, MINB, COMPAT, SMEM>;
-  const int smem = SMEM ? (int)(sizeof(double) * A.N * A.N * A.D) : 0;
+  constexpr int kSlots = (int)sizeof(GrpSmem<G, M>) * kGWarps * (32 / G);
+  const int smem = kSlots + (SMEM ? (int)(sizeof(double) * A.N * A.N * A.D) : 0);
   static thread_local int cap_for = -1, cap = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (cap_for != dev) {
-    if (SMEM) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvalSmemMax);
+    const int most = kSlots + (SMEM ? kEvalSmemMax : 0);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * kGWarps, SMEM ? kEvalSmemMax : 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * kGWarps, most);
     cap = sms * (per > 0 ? per : 1);
     cap_for = dev;
   }
@@ -462,12 +467,15 @@ int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s) {
   if (n == 0) return HOI_OK;
   const bool compat = A.logdet || A.invdiag;
   const bool smem = sizeof(double) * A.N * A.N * A.D <= (size_t)kEvalSmemMax;
-  // (G, M) per order range, measured on B200 (cfg4 order segments, TF/s):
-  // K 17-18 (2,9) 3.2-3.7 | 19-20 (4,5) 3.8-4.3 | 21-24 (4,6) 3.9-4.9 |
-  // 25-28 (4,7) 3.1 (a little spilled, still 20% over (8,4)) | 29-32 (8,4).
-  // (8,3) for 21-24 ran 2.7-3.4; the warp-per-unit kernel 0.8-1.5.
+  // (G, M) per order range, measured on B200 (cfg4 order segments, round 1
+  // TF/s): K 17-18 (2,9) 3.2-3.7 | 21-24 (4,6) 3.9-4.9 | 25-28 (4,7) 3.1 (a
+  // little spilled, still 20% over (8,4)) | 29-32 (8,4); (8,3) for 21-24 ran
+  // 2.7-3.4, the warp-per-unit kernel 0.8-1.5.  Round 2 (segment ms): fewer,
+  // fatter threads win while the rows fit -- K 17-18 (2,9) 2.52 vs (4,5)
+  // 3.87; K 19-20 (2,10) 3.34 vs (4,5) 4.11 (its exchange slots need the
+  // dynamic shared memory above); K 21-22 (2,11) 5.85 vs (4,6) 5.60.
   if (K <= 18) return pick_grp<2, 9, 1>(A, K, compat, smem, s);
-  if (K <= 20) return pick_grp<4, 5, 1>(A, K, compat, smem, s);
+  if (K <= 20) return pick_grp<2, 10, 1>(A, K, compat, smem, s);
   if (K <= 24) return pick_grp<4, 6, 1>(A, K, compat, smem, s);
   if (K <= 28) return pick_grp<4, 7, 1>(A, K, compat, smem, s);
   return pick_grp<8, 4, 1>(A, K, compat, smem, s);
