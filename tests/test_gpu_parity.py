@@ -338,7 +338,7 @@ def _random_cov(n, seed):
     return r * np.outer(d, d)
 
 
-@pytest.mark.parametrize("k", [17, 19, 20, 21, 24, 25, 29, 32])
+@pytest.mark.parametrize("k", [17, 18, 19, 20, 21, 22, 23, 24, 25, 29, 32])
 def test_mid_orders_vs_oracle(oracle, k):
     """Orders 17..32 (the G-threads-per-unit kernels, KT = 20 / 24 / 32 with
     identity padding): index batches over 3 datasets with non-unit variances,
