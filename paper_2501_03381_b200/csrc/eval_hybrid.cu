@@ -1,4 +1,4 @@
-// Engine 1, orders 17..22: one thread per (n-plet, dataset) unit with a
+// Engine 1, orders 17..23: one thread per (n-plet, dataset) unit with a
 // bordered LDL^T, so the register file holds only the leading KR x KR block.
 //
 // A K = 17..20 packed triangle (153-210 doubles) does not fit in 255
@@ -329,13 +329,15 @@ int launch_eval_hybrid(const EvalArgs &A, int K, cudaStream_t s) {
     // 11.1, 15 x 96 11.4 (19.2); K = 22: 15 x 64 6.8, 16 x 96 7.0 (8.2).
     // The scratch (TT KR + TT (TT + 1) / 2 doubles per thread) bounds the
     // CTAs per SM; KR = 14 spills ~0.5 KB, which costs less than the
-    // bigger tail of a smaller KR.
+    // bigger tail of a smaller KR.  Orders 14-16 stay on the register
+    // kernel (K = 16: 28.8 ms there, 30.4 bordered at KR = 13 or 14).
     case 17: return launch_hyb<17, 14, 128>(A, s);
     case 18: return launch_hyb<18, 14, 128>(A, s);
     case 19: return launch_hyb<19, 14, 128>(A, s);
     case 20: return launch_hyb<20, 14, 128>(A, s);
     case 21: return launch_hyb<21, 16, 128>(A, s);
     case 22: return launch_hyb<22, 15, 64>(A, s);
+    case 23: return launch_hyb<23, 16, 64>(A, s);   // 2.73 ms (group 3.03)
     default: return -1;
   }
 }

@@ -452,6 +452,6 @@ int launch_eval_k13_16(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_generic(const EvalArgs &A, int K, cudaStream_t s);
 int launch_eval_group(const EvalArgs &A, int K, cudaStream_t s);  // 17 <= K <= 32
 int launch_eval_pipe(const EvalArgs &A, int K, cudaStream_t s);   // 4 <= K <= 12, R in L2
-int launch_eval_hybrid(const EvalArgs &A, int K, cudaStream_t s); // 17 <= K <= 22, FP64 measures
+int launch_eval_hybrid(const EvalArgs &A, int K, cudaStream_t s); // 17 <= K <= 23, FP64 measures
 
 }  // namespace hoib

@@ -15,7 +15,7 @@ int launch_eval(const EvalArgs &A, int K, cudaStream_t s) {
   }
   else if (K <= 16) st = launch_eval_k13_16(A, K, s);
   else if (K <= 32) {
-    st = launch_eval_hybrid(A, K, s);          // K <= 22: bordered LDL^T (eval_hybrid.cu)
+    st = launch_eval_hybrid(A, K, s);          // K <= 23: bordered LDL^T (eval_hybrid.cu)
     if (st < 0) st = launch_eval_group(A, K, s);   // G threads per unit (eval_group.cu)
   }
   return st >= 0 ? st : launch_eval_generic(A, K, s);

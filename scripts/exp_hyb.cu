@@ -3,9 +3,11 @@
 // kernel and the bordered one-thread-per-unit kernel (eval_hybrid.cu).
 //   nvcc ... -I include scripts/exp_hyb.cu paper_2501_03381_b200/csrc/common.cu
 #include "../paper_2501_03381_b200/csrc/eval_group.cu"
+#include "../paper_2501_03381_b200/csrc/eval_k13_16.cu"
 #include "../paper_2501_03381_b200/csrc/eval_hybrid.cu"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -41,7 +43,8 @@ int main(int argc, char **argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int K = 17; K <= 22; ++K) {
+  const int k0 = argc > 1 ? atoi(argv[1]) : 17, k1 = argc > 2 ? atoi(argv[2]) : 22;
+  for (int K = k0; K <= k1; ++K) {
     const int64_t B = (int64_t)binom_h(30, K);
     EvalArgs A{};
     A.src = dR; A.N = N; A.D = D; A.B = B; A.r0 = 0; A.plane = B;
@@ -60,7 +63,7 @@ int main(int argc, char **argv) {
       printf("K=%d %-6s %8.3f ms  %6.2f TF/s  %s\n", K, name, ms, B * F / (ms * 1e-3) / 1e12,
              cudaGetErrorString(cudaGetLastError()));
     };
-    timeit("group", [&] { A.out = o1; launch_eval_group(A, K, 0); });
+    timeit("base", [&] { A.out = o1; if (K <= 16) launch_eval_k13_16(A, K, 0); else launch_eval_group(A, K, 0); });
     cudaMemset(o2, 0, 4 * B * 8);
     timeit("hybrid", [&] { A.out = o2; launch_eval_hybrid(A, K, 0); });
     cudaDeviceSynchronize();

@@ -36,7 +36,7 @@ def _cov(n, seed):
     return 0.5 * (s + s.T)
 
 
-@pytest.mark.parametrize("k", [17, 18, 19, 20, 21, 22])
+@pytest.mark.parametrize("k", [17, 18, 19, 20, 21, 22, 23])
 def test_hybrid_orders_global_R_vs_oracle(oracle, k):
     n, d, t = 80, 2, 1500
     sig = np.stack([_cov(n, 500 + 7 * k + s) for s in range(d)])
