@@ -61,7 +61,7 @@ constexpr int kRingLean = 6;
 constexpr int kLogBits = 8;                  // fast_log table index bits
 constexpr int kLogTab = 1 << kLogBits;
 constexpr int kLogRep = 8;                   // bank-private replicas in shared memory
-__constant__ double2 c_logtab[kLogTab];      // (c_j, L_j) of fast_log
+__device__ double2 g_logtab[kLogTab];        // (c_j, L_j) of fast_log (copied to shared per CTA)
 __constant__ uint16_t c_lexrank[BLK];        // Q mask -> rank among |Q|-subsets of F
 __constant__ uint16_t c_runmask[BLK];        // run q, position t -> Q mask (runs concatenated)
 __constant__ uint16_t c_runstart[CB + 2];    // start of run q in c_runmask
@@ -180,17 +180,42 @@ struct Leaf<0, SW> {
 };
 
 // One Schur step on a symmetric matrix kept as its lower triangle (row
-// stride ld): eliminate pivot j, A[i][l] -= A[i][j] A[l][j] / A[j][j] for
-// j < l <= i < n.  Thread t of `nt` (nt a multiple of 32) owns column
-// j+1 + (t & 31) and every (nt/32)-th row below the diagonal -- no integer
-// division, only the triangle that later steps read.
-__device__ __forceinline__ void schur_lower(double *A, int ld, int n, int j, int t, int nt) {
-  const double rp = __drcp_rn(A[j * ld + j]);
-  const int l = j + 1 + (t & 31);
-  if (l < n) {
-    const double alj = A[l * ld + j] * rp;
-#pragma unroll 4
-    for (int i = l + (t >> 5); i < n; i += nt >> 5) A[i * ld + l] = fma(-A[i * ld + j], alj, A[i * ld + l]);
+// stride ld): eliminate pivot j, D[i][l] = S[i][l] - S[i][j] (S[l][j] / S[j][j])
+// for j < l <= i < n (S == D in place, or S -> D for a step that also
+// copies).  The trailing triangle is flattened: entry e (row-major lower
+// triangle of the (n-1-j)-square trailing block) goes to thread e mod nt, so
+// every thread updates at most SLOTS independent entries -- the row-major
+// enumeration of a smaller trailing block is a prefix of the larger one's,
+// so a thread's (row, column) offsets are fixed for the whole elimination.
+// (Round 2 first form: thread = column, loop over its rows -- a triangle of
+// serial loads, the table kernel's top stall source in ncu.)  Same
+// arithmetic per entry as before (__drcp_rn pivot, alj = S[l][j] * rp, one
+// fma), so the table is bit-identical.
+// slot = e | ti << 10 | tl << 16 (e < 1024, ti, tl < 32): one register
+__device__ __forceinline__ int tri_slot(int e) {
+  int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= e) ++i;
+  while (i * (i + 1) / 2 > e) --i;
+  return e | (i << 10) | ((e - i * (i + 1) / 2) << 16);
+}
+template <int SLOTS>
+__device__ __forceinline__ void schur_flat(const double *S, double *Dst, int ld, int n, int j,
+                                           const int (&sl)[SLOTS]) {
+  const double rp = __drcp_rn(S[j * ld + j]);
+  const int sz = n - 1 - j, T = sz * (sz + 1) / 2;
+  double v[SLOTS];
+#pragma unroll
+  for (int k = 0; k < SLOTS; ++k) {
+    if ((sl[k] & 1023) < T) {
+      const int i = j + 1 + ((sl[k] >> 10) & 31), l = j + 1 + (sl[k] >> 16);
+      const double alj = S[l * ld + j] * rp;
+      v[k] = fma(-S[i * ld + j], alj, S[i * ld + l]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < SLOTS; ++k) {
+    if ((sl[k] & 1023) < T)
+      Dst[(j + 1 + ((sl[k] >> 10) & 31)) * ld + (j + 1 + (sl[k] >> 16))] = v[k];
   }
 }
 
@@ -213,9 +238,9 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   table += (int64_t)blockIdx.y << N;
   extern __shared__ double2 s_logtab[];            // kLogTab x kLogRep entries (dynamic: 32 KB)
   constexpr int MS = MAXV + 1;
-  // per-warp matrix row stride, odd: schur_lower's lanes read column j of
-  // consecutive rows (A[i][j], i = l..), which at the even stride 16 was a
-  // 16-way bank conflict (87M excess wavefronts in round-2 ncu)
+  // per-warp matrix row stride, odd: the Schur steps' lanes read column j of
+  // consecutive rows (A[i][j]), which at the even stride 16 was a 16-way
+  // bank conflict (87M excess wavefronts in round-2 ncu)
   constexpr int WS = MAXB + CB + 1;
   __shared__ double M[MAXV * MS];                  // gathered matrix, row stride MS
   __shared__ double W[NW][2][WS * WS];             // per-warp base / work (lower triangles)
@@ -226,7 +251,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nP = N - CB;
-  for (int x = tid; x < kLogTab * kLogRep; x += NT) s_logtab[x] = c_logtab[x / kLogRep];
+  for (int x = tid; x < kLogTab * kLogRep; x += NT) s_logtab[x] = __ldg(&g_logtab[x / kLogRep]);
   if (tid == 0) {
     int nf = 0;
     for (int j = b; j < nP; ++j)
@@ -242,6 +267,10 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
     if (lane <= i) M[i * MS + lane] = corr[((int64_t)vars[i] * N + vars[lane]) * D + dd];
   __syncthreads();
   // eliminate the fixed prefix variables (right-looking, lower triangle)
+  constexpr int CS = (MAXV * (MAXV - 1) / 2 + NT - 1) / NT;   // CTA slots per thread
+  int csl[CS];
+#pragma unroll
+  for (int k = 0; k < CS; ++k) csl[k] = tri_slot(tid + NT * k);
   double m0 = 1.0;
   int e0 = 0;
   for (int j = 0; j < nfix; ++j) {
@@ -250,7 +279,7 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
       if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(m0, e0, p);
     }
-    schur_lower(M, MS, m, j, tid, NT);
+    schur_flat<CS>(M, M, MS, m, j, csl);
     __syncthreads();
   }
   if (tid == 0) {
@@ -265,6 +294,9 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   double *Wb = W[warp][0], *Wm = W[warp][1];
   __shared__ double s_mb[NW];
   __shared__ int s_eb[NW];
+  // warp slots per lane (recomputed where used: kept live across the leaf
+  // recursion they spilled)
+  constexpr int WSL = ((MAXB + CB) * (MAXB + CB - 1) / 2 + 31) / 32;
   const int ulo = warp & ((1 << blo) - 1);
   if (warp < (1 << blo)) {
     double mb = s_m0;
@@ -272,12 +304,15 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
     for (int i = 0; i < w; ++i)
       if (lane <= i) Wb[i * WS + lane] = S0[i * MS + lane];
     __syncwarp();
+    int wsl[WSL];
+#pragma unroll
+    for (int k = 0; k < WSL; ++k) wsl[k] = tri_slot(lane + 32 * k);
     for (int j = 0; j < blo; ++j) {
       if (!((ulo >> j) & 1)) continue;             // warp-uniform
       const double p = Wb[j * WS + j];
       if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(mb, ebase, p);
-      schur_lower(Wb, WS, w, j, lane, 32);
+      schur_flat<WSL>(Wb, Wb, WS, w, j, wsl);
       __syncwarp();
     }
     if (lane == 0) {
@@ -289,26 +324,32 @@ k_lattice_table(const double *__restrict__ corr, int N, int D, int d, int b,
   for (int uh = 0; uh < (1 << (b - blo)); ++uh) {
     if (warp >= (1 << blo)) break;
     const int u = ulo | (uh << blo);
-    for (int i = 0; i < w; ++i)
-      if (lane <= i) Wm[i * WS + lane] = Wb[i * WS + lane];
-    __syncwarp();
     double mu = s_mb[warp];
     int eu = s_eb[warp];
+    // the pattern's first step reads the warp's base and writes the work
+    // matrix's trailing triangle (every entry later steps and the suffix
+    // read), so no copy of the base is made; a pattern without set bits
+    // here reads the base directly
+    const double *Sw = Wb;
+    int wsl[WSL];
+#pragma unroll
+    for (int k = 0; k < WSL; ++k) wsl[k] = tri_slot(lane + 32 * k);
     for (int j = blo; j < b; ++j) {
       if (!((u >> j) & 1)) continue;               // warp-uniform
-      const double p = Wm[j * WS + j];
+      const double p = Sw[j * WS + j];
       if (!(p > kMinPivot)) s_bad = 1;
       lp_mul(mu, eu, p);
-      schur_lower(Wm, WS, w, j, lane, 32);
+      schur_flat<WSL>(Sw, Wm, WS, w, j, wsl);
       __syncwarp();
+      Sw = Wm;
     }
-    // suffix Schur complement C = Wm[b.., b..] (CB x CB); each lane takes
+    // suffix Schur complement C = Sw[b.., b..] (CB x CB); each lane takes
     // the lower triangle into registers and eliminates its F0..F4 pattern
     double c[CB * (CB + 1) / 2];
 #pragma unroll
     for (int i = 0; i < CB; ++i)
 #pragma unroll
-      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = Wm[(b + i) * WS + (b + l)];
+      for (int l = 0; l <= i; ++l) c[i * (i + 1) / 2 + l] = Sw[(b + i) * WS + (b + l)];
     __syncwarp();
     double ml = mu;
     int el = eu;
@@ -1258,7 +1299,7 @@ void upload_tables() {
     lt[j].x = cd;
     lt[j].y = (double)(-logl((long double)cd));
   }
-  cudaMemcpyToSymbol(c_logtab, lt.data(), sizeof(double2) * kLogTab);
+  cudaMemcpyToSymbol(g_logtab, lt.data(), sizeof(double2) * kLogTab);
   cudaMemcpyToSymbol(g_runmask, rm.data(), sizeof(uint16_t) * BLK);
   {
     std::vector<uint32_t> gr(BLK);
