@@ -315,9 +315,11 @@ int launch_hyb(const EvalArgs &A, cudaStream_t st) {
 }  // namespace
 
 // -1 when the launch is not this kernel's: FP64 measures only (no
-// entropy_terms outputs, no raw matrix stacks, no FP32 path).
+// entropy_terms outputs, no raw matrix stacks).  precision="fp32" requests
+// run here in FP64 too, as they do on every kernel above order 16, so the
+// two precisions give identical values at these orders.
 int launch_eval_hybrid(const EvalArgs &A, int K, cudaStream_t s) {
-  if (A.mats || A.fp32 || A.logdet || A.invdiag || !A.out) return -1;
+  if (A.mats || A.logdet || A.invdiag || !A.out) return -1;
   if (A.B * (int64_t)A.D == 0) return HOI_OK;
   upload_binomials();
   switch (K) {

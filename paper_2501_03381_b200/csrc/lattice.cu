@@ -1056,17 +1056,25 @@ k_lattice_measures(const double *__restrict__ table, int N, int D, int d, int km
 // CTA at 53 KB of shared memory: 4 CTAs per SM.
 constexpr int kRingOwn = 3;
 
-struct FullSmem {
-  double ring[kRingOwn][BLK];
+template <int RING, bool NBS>
+struct FullSmemT {
+  double ring[RING][BLK];
   double own[2][BLK];
-  double nbs[BLK];
+  double nbs[NBS ? BLK : 1];
   uint32_t run[BLK];
-  uint64_t full[kRingOwn];
-  uint64_t empty[kRingOwn];
+  uint64_t full[RING];
+  uint64_t empty[RING];
   uint64_t own_full[2];
   uint64_t own_empty[2];
   int64_t base[2][CB + 1];
 };
+// HOLD (the FAST instantiation, whose blocks always carry the pass-1-sum
+// job): no separate neighbour-sum buffer; a block's last ring job is not
+// released after it is accumulated, the block's neighbour sums are written
+// over it (each thread over the very pairs it read) and the slot is freed
+// after the epilogue.  The 8 KB buy a 4th ring slot at the same 4 CTAs/SM.
+template <bool HOLD>
+using FullSmem = FullSmemT<HOLD ? 4 : kRingOwn, !HOLD>;
 
 // FAST: one dataset, no bias, the whole rank range, global rows -- the
 // headline configuration -- with every branch of the general epilogue
@@ -1080,7 +1088,9 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
                unsigned blk_begin, unsigned blk_end, const uint8_t *__restrict__ active,
                unsigned *__restrict__ counter, StencilPass ps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  FullSmem &sm = *reinterpret_cast<FullSmem *>(smem_raw);
+  constexpr bool HOLD = FAST;
+  constexpr int RING = HOLD ? 4 : kRingOwn;
+  FullSmem<HOLD> &sm = *reinterpret_cast<FullSmem<HOLD> *>(smem_raw);
   __shared__ unsigned blkq[kBlkQ];
   __shared__ unsigned blkc[kBlkQ];
   constexpr uint32_t kBlkBytes = BLK * sizeof(double);
@@ -1091,7 +1101,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
     sm.run[p] = (uint32_t)e | ((uint32_t)(p - c_runstart[q]) << 10) | ((uint32_t)q << 20);
   }
   if (tid == 0) {
-    for (int s = 0; s < kRingOwn; ++s) {
+    for (int s = 0; s < RING; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kConsumerWarps);
     }
@@ -1146,8 +1156,8 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       unsigned prem = P & nbmask;
       bool extra = ps.extra != nullptr;
       while (extra || prem) {
-        const int slot = pJ % kRingOwn;
-        if (pJ >= kRingOwn) mbar_wait(&sm.empty[slot], ((pJ / kRingOwn) - 1) & 1u);
+        const int slot = pJ % RING;
+        if (pJ >= RING) mbar_wait(&sm.empty[slot], ((pJ / RING) - 1) & 1u);
         const double *srcp;
         if (extra) {                               // DRAM-sourced: first
           srcp = ps.extra + (int64_t)P * BLK;
@@ -1192,9 +1202,10 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
     double2 acc[PAIRS];
 #pragma unroll
     for (int r = 0; r < PAIRS; ++r) acc[r] = make_double2(0.0, 0.0);
+    int hslot = 0;
     for (int m = 0; m < nj; ++m, ++J) {
-      const int slot = J % kRingOwn;
-      mbar_wait(&sm.full[slot], (J / kRingOwn) & 1u);
+      const int slot = J % RING;
+      mbar_wait(&sm.full[slot], (J / RING) & 1u);
       const double *src = sm.ring[slot];
 #pragma unroll
       for (int r = 0; r < PAIRS; ++r) {
@@ -1202,10 +1213,14 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
         acc[r].x += v.x;
         acc[r].y += v.y;
       }
-      release_slot(&sm.empty[slot], lane);
+      if (HOLD && m == nj - 1)
+        hslot = slot;                              // kept: becomes this block's nbs
+      else
+        release_slot(&sm.empty[slot], lane);
     }
     const double *own = sm.own[buf];
-    if (seq > 0) named_bar_sync(2, kStencilThreads);   // previous epilogue done with nbs
+    double *nbs = HOLD ? sm.ring[hslot] : sm.nbs;
+    if (!HOLD && seq > 0) named_bar_sync(2, kStencilThreads);   // previous epilogue done with nbs
 #pragma unroll
     for (int r = 0; r < PAIRS; ++r) {
       const int e0 = 2 * (tid + kStencilThreads * r);
@@ -1223,7 +1238,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
           s1 += f ? v.x : v.y;
         }
       }
-      *reinterpret_cast<double2 *>(sm.nbs + pw[r]) = flip[r] ? make_double2(s1, s0) : make_double2(s0, s1);
+      *reinterpret_cast<double2 *>(nbs + pw[r]) = flip[r] ? make_double2(s1, s0) : make_double2(s0, s1);
     }
     named_bar_sync(1, kStencilThreads);           // nbs and base[buf] complete
 #pragma unroll
@@ -1235,7 +1250,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       const int64_t row = (!FAST && ps.local) ? lrow0 + tid + kStencilThreads * r : b0 + t;
       const bool valid = b0 != kNoRun && (FAST || ps.local || (row >= 0 && row < rows));
       if (!valid) continue;
-      const double l = own[swz(e)], nb = sm.nbs[swz(e)];
+      const double l = own[swz(e)], nb = nbs[swz(e)];
       const double kd = (double)k;
       double tc, dtc, o;
       if (!FAST && et) {
@@ -1256,6 +1271,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       __stcs(out + 2 * plane + oi, o);
       __stcs(out + 3 * plane + oi, tc + dtc);
     }
+    if (HOLD) release_slot(&sm.empty[hslot], lane);   // the held job slot
     release_slot(&sm.own_empty[buf], lane);       // own block free for block seq + 2
   }
 }
@@ -1584,7 +1600,7 @@ static int run_full_t(const LatticeWs &w, int N, int D, int d, const double *eta
   static thread_local int grid_cap = 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int smem = (int)sizeof(FullSmem);
+  const int smem = (int)sizeof(FullSmem<FAST>);
   if (set_for != dev) {
     cudaFuncSetAttribute(k_lattice_full<FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int sms = 0, per_sm = 0;
@@ -1610,7 +1626,9 @@ static int run_full(const LatticeWs &w, int N, int D, int d, const double *eta, 
                     const StencilPass &ps, cudaStream_t s) {
   int64_t h_off[MAXV + 1];
   const bool whole = g_begin == 0 && g_end == total_rows(N, kmin, kmax, h_off);
-  if (D == 1 && !eta && whole && !ps.local && ps.nstack == 0)
+  // FAST holds each block's last ring job (its pass-1-sum job at least: the
+  // two-pass split) as the neighbour-sum buffer, so it needs ps.extra
+  if (D == 1 && !eta && whole && !ps.local && ps.nstack == 0 && ps.extra)
     return run_full_t<true>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
                             blk_begin, blk_end, active, ps, s);
   return run_full_t<false>(w, N, D, d, eta, kstride, kmin, kmax, g_begin, g_end, out, plane,
