@@ -2,7 +2,7 @@
 # runs the lattice-only bench line alternately (new, old, new, old).
 L=paper_2501_03381_b200/_lib/libhoib200.so
 cp $L /tmp/lib_new.so
-for r in 1 2; do
+for r in ${ROUNDS:-1 2}; do
   for v in new old; do
     if [ $v = new ]; then cp /tmp/lib_new.so $L; else cp $1 $L; fi
     touch $L
