@@ -1114,6 +1114,17 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
   __syncthreads();
   const unsigned nbmask = ps.nbmask;
   const int nP = N - CB;
+  // FAST block pairs: a CTA claims two consecutive claim indices, i.e. the
+  // blocks P and P | pbit (pbit = the lowest high prefix bit, the claim
+  // order varies it fastest).  P is the pair's second block's neighbour
+  // over pbit, and it is already on chip as the first block's own block, so
+  // that neighbour job is not streamed: the second block adds it from the
+  // other own buffer (last, where far-bits-first order puts pbit), and the
+  // first block's own buffer is freed after that instead of after its own
+  // epilogue.  One ring job per pair fewer.
+  const bool pair = FAST && ps.perm_lb > 0 && ((nbmask >> ps.perm_lb) & 1u) &&
+                    (((blk_end - blk_begin) & 1u) == 0) && !active && !ps.list && ps.nstack == 0;
+  const unsigned pbit = pair ? (1u << ps.perm_lb) : 0u;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------ producer ----
@@ -1139,12 +1150,32 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       }
     };
     uint32_t pJ = 0;
+    unsigned Pnext = kEndBlock, cnext = 0;
     for (uint32_t seq = 0;; ++seq) {
-      const unsigned Pg = claim();
+      unsigned Pg, cg;
+      if (pair) {
+        if ((seq & 1) == 0) {
+          c = atomicAdd(counter, 2u);
+          if (c >= blk_end - blk_begin) {
+            Pg = kEndBlock;
+          } else {
+            Pg = blk_begin + (((c & ((1u << hb) - 1u)) << ps.perm_lb) | (c >> hb));
+            Pnext = Pg | pbit;
+            cnext = c + 1;
+          }
+          cg = c;
+        } else {
+          Pg = Pnext;
+          cg = cnext;
+        }
+      } else {
+        Pg = claim();
+        cg = c;
+      }
       const int ob = seq & 1;
       if (seq >= 2) mbar_wait(&sm.own_empty[ob], ((seq >> 1) - 1) & 1u);
       blkq[seq % kBlkQ] = Pg;                      // published by the own-block arrival
-      blkc[seq % kBlkQ] = c;
+      blkc[seq % kBlkQ] = cg;
       if (Pg == kEndBlock) {
         mbar_arrive(&sm.own_full[ob]);             // tx-free arrival: the end marker
         return;
@@ -1154,6 +1185,7 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       mbar_expect_tx(&sm.own_full[ob], kBlkBytes);
       tma_load_1d(sm.own[ob], tab + (int64_t)P * BLK, kBlkBytes, &sm.own_full[ob], pol_own);
       unsigned prem = P & nbmask;
+      if (pair && (seq & 1)) prem &= ~pbit;         // the pair's first block, on chip
       bool extra = ps.extra != nullptr;
       while (extra || prem) {
         const int slot = pJ % RING;
@@ -1197,7 +1229,8 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
     const double *et = eta ? eta + (int64_t)dd * kstride : nullptr;
     const double e1 = et ? et[1] : 0.0;
     const int kP = __popc(P);
-    const int nj = __popc(P & nbmask) + (ps.extra ? 1 : 0);
+    const bool second = pair && (seq & 1);
+    const int nj = __popc(P & nbmask) + (ps.extra ? 1 : 0) - (second ? 1 : 0);
     if (tid <= CB) sm.base[buf][tid] = run_base(P, tid, N, kmin, kmax, order_off, g_begin);
     double2 acc[PAIRS];
 #pragma unroll
@@ -1217,6 +1250,16 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
         hslot = slot;                              // kept: becomes this block's nbs
       else
         release_slot(&sm.empty[slot], lane);
+    }
+    if (second) {                                  // neighbour over pbit: the first block
+      const double *po = sm.own[buf ^ 1];
+#pragma unroll
+      for (int r = 0; r < PAIRS; ++r) {
+        const double2 v = *reinterpret_cast<const double2 *>(po + pw[r]);
+        acc[r].x += v.x;
+        acc[r].y += v.y;
+      }
+      release_slot(&sm.own_empty[buf ^ 1], lane);
     }
     const double *own = sm.own[buf];
     double *nbs = HOLD ? sm.ring[hslot] : sm.nbs;
@@ -1272,7 +1315,8 @@ k_lattice_full(const double *__restrict__ table, int N, int D, int d, int kmin, 
       __stcs(out + 3 * plane + oi, tc + dtc);
     }
     if (HOLD) release_slot(&sm.empty[hslot], lane);   // the held job slot
-    release_slot(&sm.own_empty[buf], lane);       // own block free for block seq + 2
+    if (!pair || (seq & 1))                       // a pair's first block: freed by the second
+      release_slot(&sm.own_empty[buf], lane);     // own block free for block seq + 2
   }
 }
 
