@@ -228,8 +228,15 @@ __device__ __noinline__ bool hyb_retry(const double *__restrict__ src, const Eva
   return hyb_unit<K, KR, NT, true>(src, A, d, s, x, 1e-10 * tr / (double)K, l, lam);
 }
 
+// resident threads per SM the register budget targets (2 CTAs of 128).
+// 384 (a 170-register cap, 12 warps/SM with 64-thread CTAs) measured
+// 45-53 ms for order 17 against 29.5 at 256: the spills cost more than the
+// extra warps hide (scripts/exp_hyb.cu -DHYB_OCC=384 -DHYB_VARIANTS).
+#ifndef HYB_OCC
+#define HYB_OCC 256
+#endif
 template <int K, int KR, int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, 256 / NT) k_eval_hyb(const EvalArgs A) {
+__global__ void __launch_bounds__(NT, HYB_OCC / NT) k_eval_hyb(const EvalArgs A) {
   constexpr int TT = K - KR;
   extern __shared__ __align__(16) unsigned char hyb_raw[];
   double *x = reinterpret_cast<double *>(hyb_raw) + threadIdx.x;

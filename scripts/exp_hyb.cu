@@ -65,6 +65,20 @@ int main(int argc, char **argv) {
     };
     timeit("base", [&] { A.out = o1; if (K <= 16) launch_eval_k13_16(A, K, 0); else launch_eval_group(A, K, 0); });
     cudaMemset(o2, 0, 4 * B * 8);
+#ifdef HYB_VARIANTS
+    if (K == 17) {
+      timeit("kr10", [&] { A.out = o2; launch_hyb<17, 10, 128>(A, 0); });
+      timeit("kr11", [&] { A.out = o2; launch_hyb<17, 11, 128>(A, 0); });
+      timeit("kr12", [&] { A.out = o2; launch_hyb<17, 12, 128>(A, 0); });
+      timeit("kr12x64", [&] { A.out = o2; launch_hyb<17, 12, 64>(A, 0); });
+      timeit("kr11x64", [&] { A.out = o2; launch_hyb<17, 11, 64>(A, 0); });
+      timeit("kr13x64", [&] { A.out = o2; launch_hyb<17, 13, 64>(A, 0); });
+    } else if (K == 18) {
+      timeit("kr12x64", [&] { A.out = o2; launch_hyb<18, 12, 64>(A, 0); });
+      timeit("kr11", [&] { A.out = o2; launch_hyb<18, 11, 128>(A, 0); });
+      timeit("kr12", [&] { A.out = o2; launch_hyb<18, 12, 128>(A, 0); });
+    }
+#endif
     timeit("hybrid", [&] { A.out = o2; launch_eval_hybrid(A, K, 0); });
     cudaDeviceSynchronize();
     std::vector<double> h1(4 * B), h2(4 * B);
