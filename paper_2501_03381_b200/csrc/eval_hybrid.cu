@@ -1,7 +1,7 @@
 // Engine 1, orders 17..23: one thread per (n-plet, dataset) unit with a
 // bordered LDL^T, so the register file holds only the leading KR x KR block.
 //
-// A K = 17..20 packed triangle (153-210 doubles) does not fit in 255
+// A K = 17..23 packed triangle (153-276 doubles) does not fit in 255
 // registers: the fixed-K register kernel spills kilobytes per thread and the
 // group kernel (eval_group.cu) splits a unit over G threads that exchange
 // every column through shared memory.  Here the factorisation is reordered
@@ -12,7 +12,8 @@
 //                the thread's shared-memory scratch, conflict-free
 //                [entry][thread] layout), Schur column
 //                c_ii' = a_ii' - z . l_i'  for the tail rows i' <= i
-//   C = A22 - L21 D1 L21^T = L22 D2 L22^T (registers, TT = K - KR small)
+//   C = A22 - L21 D1 L21^T = L22 D2 L22^T (TT = K - KR rows; factorised in
+//                the shared scratch too, beside the multipliers)
 //   U = L^-1:  U11 = L11^-1, U22 = L22^-1 in place, U21 = -U22 (L21 U11)
 //   (R_S^-1)_jj = sum_i U_ij^2 / d_i over both blocks.
 //
@@ -23,11 +24,14 @@
 // failure rule as k_eval (ref measures.py:41-81, nplet_engine.py:237-264): a
 // non-positive pivot reruns the unit with the jittered diagonal, a second
 // failure records (row, dataset) and writes NaN.
+//
+// The loops over tail rows are deliberately not unrolled: unrolled, the
+// scheduler interleaved the rows and kept all their gathers and partial
+// sums live (3-5 KB of spills per thread); rolled, KR = 14 spills ~0.5 KB.
 #include "eval_kernels.cuh"
 
 namespace hoib {
 namespace {
-
 
 __device__ __forceinline__ int opaque_zero(double v) {
   int z;
