@@ -422,16 +422,19 @@ def test_lattice_matches_percell_engine_cfg3(golden):
         assert bool((a[3] == a[0] + a[1]).all())
 
 
-@pytest.mark.parametrize("n", [26, 28])
-def test_lattice_column_pass_splits_vs_percell(n):
-    """Two-pass full output at the column pass's other splits (N = 26: 8 low
-    prefix bits, N = 28: 9; cfg4's 10 is the every-row test) against the
-    per-n-plet engine on every row."""
+@pytest.mark.parametrize("bias", [True, False])
+@pytest.mark.parametrize("n", [24, 25, 26, 28])
+def test_lattice_column_pass_splits_vs_percell(n, bias):
+    """Two-pass full output at the column pass's other splits (N = 24/25: 7
+    low prefix bits, N = 26: 8, N = 28: 9; cfg4's 10 is the every-row test)
+    against the per-n-plet engine on every row.  Without bias the whole-range
+    scan takes the specialised pass-2 kernel (held ring job, block pairs over
+    the lowest high prefix bit); with bias the general one."""
     rng = np.random.default_rng(100 + n)
     c = 0.7 * workloads.randcorr(n, rng) + 0.3 * np.eye(n)
     covs = hoi.CovSet([hoi.CovarianceMatrix(c, n_samples_used=1000)])
-    a = hoi.scan_device(covs, 2, n, bias_correct=True, engine=2).out
-    b = hoi.scan_device(covs, 2, n, bias_correct=True, engine=1).out
+    a = hoi.scan_device(covs, 2, n, bias_correct=bias, engine=2).out
+    b = hoi.scan_device(covs, 2, n, bias_correct=bias, engine=1).out
     err = (a - b).abs() - 1e-9 * b.abs()
     assert float(err.max()) <= 1e-11
     assert bool((a[3] == a[0] + a[1]).all())
